@@ -1,0 +1,188 @@
+/*
+ * sals.h — C ABI of the B200-native SALS decode-attention hot path
+ * (Sparse Attention in Latent Space, arXiv 2510.24273).
+ *
+ * Citations: "P:n" = line n of the paper's LaTeX; "S:n" = SPEC.md.
+ *
+ * Conventions shared by every entry point
+ *  - Tensor arguments are DEVICE pointers (cudaMalloc / torch CUDA storage)
+ *    owned by the caller, row-major, 16-byte aligned, contiguous.  The
+ *    library allocates nothing and keeps no state between calls.
+ *  - `stream` is a cudaStream_t passed as void*.  Every call only enqueues
+ *    work on that stream (no host synchronisation), so all calls are CUDA-graph
+ *    capturable.  Kernels are launched with programmatic dependent launch.
+ *  - Argument errors are detected on the host and returned synchronously with
+ *    nothing enqueued.  Launch failures return SALS_ERR_CUDA; asynchronous
+ *    device faults surface at the caller's next synchronisation.
+ *    sals_last_error() returns a thread-local message for the last failure.
+ *  - Element type of U, q, k_new, v_new, caches and out is cfg->dtype
+ *    (SALS_F32 or SALS_BF16); accumulation is always fp32.
+ *  - Notation: B = batch, s_b = tokens of request b INCLUDING the
+ *    token being decoded (positions 0..s_b-1, query at s_b-1), n_q / n_kv query
+ *    / KV heads, G = n_q/n_kv (query head h reads KV head h/G), d = head_dim,
+ *    D = n_kv*d (the paper's "nd"), r = rank, r* = score_rank, k = top_k.
+ */
+#ifndef SALS_H_
+#define SALS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SALS_OK = 0,
+  SALS_ERR_INVALID_ARGUMENT = 1,   /* shape / pointer / range violation */
+  SALS_ERR_UNSUPPORTED = 2,        /* shape outside the kernels' limits (see each call) */
+  SALS_ERR_WORKSPACE_TOO_SMALL = 3,
+  SALS_ERR_CUDA = 4
+} sals_status;
+
+typedef enum { SALS_F32 = 0, SALS_BF16 = 1 } sals_dtype;
+
+/* RoPE pairing (the paper is silent): HALF rotates (i, i+d/2) (HF
+ * rotate_half), INTERLEAVED rotates (2i, 2i+1). */
+typedef enum { SALS_ROPE_HALF = 0, SALS_ROPE_INTERLEAVED = 1 } sals_rope_style;
+
+/* Reconstruction + attention path.  AUTO picks TCGEN05 when the selected-row
+ * reconstruction is a real dense contraction (bf16, B*k >= 128 rows,
+ * d in {64,128,256}, D % 256 == 0), SIMT otherwise. */
+typedef enum { SALS_PATH_AUTO = 0, SALS_PATH_SIMT = 1, SALS_PATH_TCGEN05 = 2 } sals_path;
+
+/* The problem statement of Algorithm 1: heads, head_dim, rank r,
+ * score rank r*, budget k, RoPE base, GQA grouping. */
+typedef struct {
+  int32_t num_q_heads;    /* n_q; n_q % n_kv == 0 (contiguous GQA groups)            */
+  int32_t num_kv_heads;   /* n_kv                                                     */
+  int32_t head_dim;       /* d: even, one of 16, 32, 64, 128, 256                     */
+  int32_t rank;           /* r: 1 <= r <= D, r % 8 == 0 (P:358 U_r in R^{nd x r})     */
+  int32_t score_rank;     /* r*: 1 <= r* <= r, r* % 8 == 0; paper: r* = r/2   */
+  int32_t top_k;          /* k >= 1 (Alg. 1 line 5)                                   */
+  int32_t sink;           /* x: first x positions always selected; 0 = pure Alg. 1 */
+  int32_t recent;         /* z: last z positions always selected; sink + recent <= k  */
+  float   rope_base;      /* theta base of RoPE (model config; the paper never states it) */
+  int32_t rope_style;     /* sals_rope_style                                          */
+  int32_t dtype;          /* sals_dtype of every tensor argument                      */
+  float   softmax_scale;  /* 0 => 1/sqrt(head_dim) (Alg. 1 line 8)             */
+  int32_t path;           /* sals_path                                                */
+} sals_config;
+
+/* Bytes of device workspace sals_decode needs for `batch` requests of at most
+ * `max_seq_len` tokens.  0 on invalid arguments. */
+size_t sals_workspace_bytes(const sals_config* cfg, int32_t batch, int32_t max_seq_len);
+
+/*
+ * sals_append_latent — Algorithm 1 lines 2-3 for the new token (
+ * Eq. 1): k~ = U^T k_new (fp32 accumulate, rounded to dtype) is
+ * written to latent_cache[b, d_pos[b], :], and v_new[b] to v_cache[b, d_pos[b], :].
+ *   U            [D, r]       column-orthonormal projection, columns in
+ *                             descending-eigenvalue order
+ *   k_new        [B, D]       PRE-RoPE keys of the new token
+ *   v_new        [B, D]       values of the new token
+ *   d_pos        [B] int32    device: slot (= absolute position) of the new token, 0 <= pos < cap
+ *   latent_cache [B, cap, r]  written in place (row d_pos[b] only)
+ *   v_cache      [B, cap, D]  written in place (row d_pos[b] only)
+ * Must precede sals_decode of the same step on the same stream (Alg. 1 appends
+ * before scoring).
+ */
+sals_status sals_append_latent(const sals_config* cfg, const void* U, const void* k_new,
+                               const void* v_new, int32_t batch, const int32_t* d_pos,
+                               void* latent_cache, void* v_cache, int64_t cap, void* stream);
+
+/*
+ * sals_decode — Algorithm 1 lines 2 and 4-9 for a batch of
+ * independent requests:
+ *   q~ = U[:, :r*]^T q_bar          q_bar = sum of the query heads of a KV group
+ *                                   (reading R1; = q for MHA)
+ *   p'_j = q~ . K~[b, j, :r*]        j < s_b
+ *   C_b = [0,x) u [s_b-z, s_b) u TopK over [x, s_b-z) of k-x-z tokens, ties to
+ *         the lower index; all s_b tokens when s_b <= k   (line 5)
+ *   K_C = K~[b, C_b, :] U^T, reshaped to [|C|, n_kv, d]      (line 6)
+ *   q^R = RoPE_{s_b-1}(q), K^R_C = RoPE_j(K_C) at the original positions j
+ *   y = softmax(q^R K^R_C^T * scale) V[b, C_b]                (lines 7-9, Eq. 6)
+ *   U            [D, r]
+ *   q            [B, n_q*d]       PRE-RoPE queries of the decoded token
+ *   latent_cache [B, cap, r]      rows 0..s_b-1 valid (append already done)
+ *   v_cache      [B, cap, D]
+ *   d_seq_len    [B] int32        device: s_b, 1 <= s_b <= min(cap, max_seq_len)
+ *   max_seq_len  host upper bound of every s_b (sizes grids; no device read)
+ *   out          [B, n_q*d]       attention output y
+ *   sel_idx_out  [B, k] int32 or NULL: C_b ascending, -1 padded past min(k, s_b)
+ *   scores_out   [B, max_seq_len] fp32 or NULL: p' (debug / parity)
+ *   workspace    >= sals_workspace_bytes(cfg, batch, max_seq_len) bytes, 256-B aligned
+ * Limits (SALS_ERR_UNSUPPORTED): max_seq_len <= 524288, batch <= 65535,
+ * n_q/n_kv <= 8.
+ */
+sals_status sals_decode(const sals_config* cfg, const void* U, const void* q,
+                        const void* latent_cache, const void* v_cache, int64_t cap,
+                        int32_t batch, const int32_t* d_seq_len, int32_t max_seq_len,
+                        void* out, int32_t* sel_idx_out, float* scores_out,
+                        void* workspace, size_t ws_bytes, void* stream);
+
+/*
+ * Dense full-KV comparator built in the same library (the "vs dense" baseline
+ * of the north star; FlashAttention-2 is the paper's).
+ * sals_dense_append: k_cache[b, pos] = RoPE_pos(k_new[b]) (post-RoPE cache),
+ * v_cache[b, pos] = v_new[b].
+ * sals_dense_decode: y = softmax(RoPE_{s-1}(q) K[0:s]^T * scale) V[0:s],
+ * flash-decode split over the sequence with a log-sum-exp merge.
+ */
+sals_status sals_dense_append(const sals_config* cfg, const void* k_new, const void* v_new,
+                              int32_t batch, const int32_t* d_pos, void* k_cache, void* v_cache,
+                              int64_t cap, void* stream);
+size_t sals_dense_workspace_bytes(const sals_config* cfg, int32_t batch, int32_t max_seq_len);
+sals_status sals_dense_decode(const sals_config* cfg, const void* q, const void* k_cache,
+                              const void* v_cache, int64_t cap, int32_t batch,
+                              const int32_t* d_seq_len, int32_t max_seq_len, void* out,
+                              void* workspace, size_t ws_bytes, void* stream);
+
+/*
+ * Sequence-sharded decode — the three device phases around the
+ * two exchanges.  Rank p holds the contiguous positions
+ * [shard_start, shard_start + local_len_b) of every request b.  The caller
+ * (one process per GPU) all-gathers between the phases over NCCL:
+ *  1. sals_shard_candidates: local q~, p' over the shard, and the local top
+ *     min(k-x-z, n_ranked) of the ranked range [x, s_b-z) with GLOBAL indices,
+ *     ascending index order, padded with (idx -1, score -inf) to k entries.
+ *       cand_score [B, k] fp32, cand_idx [B, k] int32 (outputs)
+ *  2. (caller) all-gather -> cand_all_* [P, B, k] in rank order.
+ *  3. sals_shard_attend: global TopK over the P*k candidates with the same
+ *     policy and tie-break as sals_decode (identical on every rank), then
+ *     reconstruct + RoPE + attention over the OWNED selected tokens (plus the
+ *     owned sink / recent ones) -> partial (m, l, o) per (b, query head):
+ *       partial [B, n_q, d+2] fp32: m (log2 domain), l, o[d]
+ *  4. (caller) all-gather -> partial_all [P, B, n_q, d+2].
+ *  5. sals_merge_partials: log-sum-exp merge -> out [B, n_q*d] (every rank).
+ * With P = 1 the result equals sals_decode's (bit-identical selection).
+ *   d_local_len [B] int32 device, d_seq_len [B] int32 device (global s_b).
+ */
+sals_status sals_shard_candidates(const sals_config* cfg, const void* U, const void* q,
+                                  const void* latent_shard, int64_t cap_local, int32_t batch,
+                                  int64_t shard_start, const int32_t* d_local_len,
+                                  int32_t max_local_len, const int32_t* d_seq_len,
+                                  float* cand_score, int32_t* cand_idx,
+                                  void* workspace, size_t ws_bytes, void* stream);
+sals_status sals_shard_attend(const sals_config* cfg, const void* U, const void* q,
+                              const void* latent_shard, const void* v_shard, int64_t cap_local,
+                              int32_t batch, int64_t shard_start, const int32_t* d_local_len,
+                              int32_t max_local_len, const int32_t* d_seq_len,
+                              const float* cand_all_score, const int32_t* cand_all_idx,
+                              int32_t world, float* partial, void* workspace, size_t ws_bytes,
+                              void* stream);
+sals_status sals_merge_partials(const sals_config* cfg, const float* partial_all, int32_t world,
+                                int32_t batch, void* out, void* stream);
+size_t sals_shard_workspace_bytes(const sals_config* cfg, int32_t batch, int32_t max_local_len,
+                                  int32_t world);
+
+const char* sals_status_string(sals_status s);
+const char* sals_last_error(void);
+/* Number of kernel launches enqueued by the calling thread since the last reset
+ * (bench.py's gpu_launches count). */
+uint64_t sals_launch_count(int32_t reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SALS_H_ */

@@ -1,0 +1,629 @@
+// Host side of the C ABI (include/sals.h): argument validation, workspace
+// carving, path / grid planning and stream-ordered launches (programmatic
+// dependent launch, thread-block clusters).  Never allocates, never syncs.
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/sals.h"
+#include "kernels.h"
+#include "recon_attn_tc.h"
+
+using namespace sals;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+sals_status fail(sals_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                   int cluster, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[2];
+  int na = 0;
+  attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[na].val.programmaticStreamSerializationAllowed = 1;
+  ++na;
+  if (cluster > 1) {
+    attrs[na].id = cudaLaunchAttributeClusterDimension;
+    attrs[na].val.clusterDim.x = cluster;
+    attrs[na].val.clusterDim.y = 1;
+    attrs[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = attrs;
+  cfg.numAttrs = na;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+#define SALS_CUDA_TRY(expr)                                                          \
+  do {                                                                               \
+    cudaError_t e_ = (expr);                                                         \
+    if (e_ != cudaSuccess) return fail(SALS_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+int next_pow2(int v) { int p = 1; while (p < v) p <<= 1; return p; }
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+sals_status validate(const sals_config* c) {
+  if (!c) return fail(SALS_ERR_INVALID_ARGUMENT, "cfg is NULL");
+  if (c->num_q_heads < 1 || c->num_kv_heads < 1 || c->num_q_heads % c->num_kv_heads)
+    return fail(SALS_ERR_INVALID_ARGUMENT, "num_q_heads (%d) must be a positive multiple of num_kv_heads (%d)",
+                c->num_q_heads, c->num_kv_heads);
+  const int G = c->num_q_heads / c->num_kv_heads;
+  if (G != 1 && G != 2 && G != 4 && G != 8) return fail(SALS_ERR_UNSUPPORTED, "GQA group %d not in {1,2,4,8}", G);
+  const int d = c->head_dim;
+  if (d != 16 && d != 32 && d != 64 && d != 128 && d != 256)
+    return fail(SALS_ERR_UNSUPPORTED, "head_dim %d not in {16,32,64,128,256}", d);
+  if (c->dtype != SALS_F32 && c->dtype != SALS_BF16) return fail(SALS_ERR_INVALID_ARGUMENT, "bad dtype %d", c->dtype);
+  if (c->dtype == SALS_F32 && d > 128) return fail(SALS_ERR_UNSUPPORTED, "fp32 supports head_dim <= 128");
+  const int D = c->num_kv_heads * d;
+  if (D > 8192) return fail(SALS_ERR_UNSUPPORTED, "n_kv*d = %d > 8192", D);
+  if (c->rank < 8 || c->rank > D || c->rank % 8)
+    return fail(SALS_ERR_INVALID_ARGUMENT, "rank %d must be a multiple of 8 in [8, D=%d]", c->rank, D);
+  if (c->score_rank < 8 || c->score_rank > c->rank || c->score_rank % 8)
+    return fail(SALS_ERR_INVALID_ARGUMENT, "score_rank %d must be a multiple of 8 in [8, rank]", c->score_rank);
+  const int epc = c->dtype == SALS_BF16 ? 8 : 4;
+  if (c->score_rank / epc > 128) return fail(SALS_ERR_UNSUPPORTED, "score_rank too large");
+  if (c->top_k < 1) return fail(SALS_ERR_INVALID_ARGUMENT, "top_k must be >= 1");
+  if (c->sink < 0 || c->recent < 0 || c->sink + c->recent > c->top_k)
+    return fail(SALS_ERR_INVALID_ARGUMENT, "need 0 <= sink, recent and sink + recent <= top_k");
+  if (!(c->rope_base > 0.f)) return fail(SALS_ERR_INVALID_ARGUMENT, "rope_base must be > 0");
+  if (c->rope_style != SALS_ROPE_HALF && c->rope_style != SALS_ROPE_INTERLEAVED)
+    return fail(SALS_ERR_INVALID_ARGUMENT, "bad rope_style");
+  if (c->softmax_scale < 0.f) return fail(SALS_ERR_INVALID_ARGUMENT, "softmax_scale must be >= 0");
+  if (c->path < SALS_PATH_AUTO || c->path > SALS_PATH_TCGEN05) return fail(SALS_ERR_INVALID_ARGUMENT, "bad path");
+  return SALS_OK;
+}
+
+RopeTable make_rope(const sals_config* c) {
+  RopeTable t{};
+  t.half = c->head_dim / 2;
+  t.style = c->rope_style;
+  for (int p = 0; p < t.half; ++p) t.theta[p] = std::pow((double)c->rope_base, -2.0 * p / c->head_dim);
+  return t;
+}
+
+float scale_log2(const sals_config* c) {
+  const float sc = c->softmax_scale > 0.f ? c->softmax_scale : 1.0f / std::sqrt((float)c->head_dim);
+  return sc * kLog2e;
+}
+
+size_t esize(const sals_config* c) { return c->dtype == SALS_BF16 ? 2 : 4; }
+
+// ---------------------------------------------------------------- planning
+struct Plan {
+  int D, G, kmax;
+  bool tc;                 // fused tcgen05 reconstruct + attention
+  int nsplit, chunk;       // flash split (SIMT) or 128-row tiles (tc)
+  int tk_cs, tk_slice;     // top-k cluster size / slice
+  size_t tk_smem;
+  int proj_cs, proj_rows;
+  // workspace offsets
+  size_t off_qtil, off_qrope, off_scores, off_sel, off_count, off_kr, off_part, total;
+  int64_t score_stride;
+};
+
+bool tc_eligible(const sals_config* c, int batch, int kmax) {
+  const int D = c->num_kv_heads * c->head_dim;
+  return c->dtype == SALS_BF16 && (int64_t)batch * kmax >= 128 && tc_supported(c->head_dim, D, c->rank,
+         c->num_q_heads / c->num_kv_heads);
+}
+
+sals_status plan_topk(int n_entries, bool cand, Plan& p) {
+  int cs = 1;
+  while (cs < 16 && ceil_div(n_entries, cs) > 2048) cs <<= 1;
+  int slice = ceil_div(n_entries, cs);
+  slice = (int)align_up(std::max(slice, 4), 4);
+  const int cap = cand ? 16384 : 32768;
+  if (slice > cap) return fail(SALS_ERR_UNSUPPORTED, "top-k over %d entries exceeds the cluster limit", n_entries);
+  p.tk_cs = cs;
+  p.tk_slice = slice;
+  p.tk_smem = (size_t)slice * 5 + 16 + (cand ? (size_t)slice * 4 : 0);
+  return SALS_OK;
+}
+
+void plan_flash(int batch, int n_kv, int ntok, int tpw_unr, int& nsplit, int& chunk) {
+  const int target = 148 * 24;
+  int ns = std::max(1, ceil_div(target, (int64_t)batch * n_kv));
+  ns = std::min(ns, std::max(1, ceil_div(ntok, tpw_unr)));
+  chunk = (int)align_up(ceil_div(ntok, ns), tpw_unr);
+  chunk = std::max(chunk, tpw_unr);
+  nsplit = std::max(1, ceil_div(ntok, chunk));
+}
+
+int flash_tpw_unr(const sals_config* c) {
+  const int epl = c->dtype == SALS_BF16 ? 8 : 4;
+  const int lpt = c->head_dim / epl;
+  return (32 / lpt) * 2;
+}
+
+sals_status make_plan(const sals_config* c, int batch, int max_s, Plan& p, bool for_size) {
+  p.D = c->num_kv_heads * c->head_dim;
+  p.G = c->num_q_heads / c->num_kv_heads;
+  p.kmax = std::min(c->top_k, max_s);
+  const bool want_tc = c->path == SALS_PATH_TCGEN05 || (c->path == SALS_PATH_AUTO);
+  p.tc = want_tc && tc_eligible(c, batch, p.kmax);
+  if (c->path == SALS_PATH_TCGEN05 && !p.tc && !for_size)
+    return fail(SALS_ERR_UNSUPPORTED, "tcgen05 path needs bf16, B*k >= 128, d in {64,128,256}, D %% 256 == 0");
+  if (p.tc) {
+    p.nsplit = ceil_div(p.kmax, kTcRows);
+    p.chunk = kTcRows;
+  } else {
+    plan_flash(batch, c->num_kv_heads, p.kmax, flash_tpw_unr(c), p.nsplit, p.chunk);
+  }
+  sals_status st = plan_topk(max_s, false, p);
+  if (st != SALS_OK) return st;
+  p.proj_cs = std::min(16, std::max(1, ceil_div(p.D, 64)));
+  p.proj_rows = ceil_div(p.D, p.proj_cs);
+  const size_t es = esize(c);
+  p.score_stride = (int64_t)align_up(max_s, 4);
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
+  p.off_qtil = take((size_t)batch * c->score_rank * 4);
+  p.off_qrope = take((size_t)batch * c->num_q_heads * c->head_dim * 4);
+  p.off_scores = take((size_t)batch * p.score_stride * 4);
+  p.off_sel = take((size_t)batch * c->top_k * 4);
+  p.off_count = take((size_t)batch * 4);
+  p.off_kr = take(p.tc ? 0 : (size_t)batch * c->top_k * p.D * es);
+  p.off_part = take((size_t)batch * c->num_q_heads * p.nsplit * (c->head_dim + 2) * 4);
+  p.total = off;
+  return SALS_OK;
+}
+
+// ------------------------------------------------------------ dispatchers
+template <typename T>
+sals_status launch_project(const sals_config* c, const Plan& p, bool pool, ProjectArgs& a, int ncols,
+                           cudaStream_t st) {
+  a.rows_per_cta = p.proj_rows;
+  const int ncolblk = ceil_div(ncols, 64);
+  dim3 grid(p.proj_cs, ncolblk + (pool ? 1 : 0));
+  if (pool) SALS_CUDA_TRY(launch(project_kernel<T, true>, grid, dim3(128), 0, st, p.proj_cs, a));
+  else SALS_CUDA_TRY(launch(project_kernel<T, false>, grid, dim3(128), 0, st, p.proj_cs, a));
+  return SALS_OK;
+}
+
+template <typename T>
+sals_status launch_score(const sals_config* c, ScoreArgs a, int batch, int max_len, cudaStream_t st) {
+  const int epc = sizeof(T) == 2 ? 8 : 4;
+  const int V = c->score_rank / epc;
+  int LG, CPL;
+  if (V <= 32) { LG = next_pow2(V); CPL = 1; }
+  else if (V <= 64) { LG = 32; CPL = 2; }
+  else { LG = 32; CPL = 4; }
+  const int tpw = 32 / LG;
+  const int unr = CPL == 1 ? 8 : (CPL == 2 ? 4 : 2);
+  const int step = 8 * tpw * unr;
+  const int64_t work = (int64_t)batch * max_len;
+  int tpc = (int)align_up(std::max<int64_t>(step, (work + 599) / 600), step);
+  a.tokens_per_cta = tpc;
+  dim3 grid(std::max(1, ceil_div(max_len, tpc)), batch);
+  void (*k)(ScoreArgs) = nullptr;
+  switch (LG * 10 + CPL) {
+    case 11: k = latent_score_kernel<T, 1, 1>; break;
+    case 21: k = latent_score_kernel<T, 2, 1>; break;
+    case 41: k = latent_score_kernel<T, 4, 1>; break;
+    case 81: k = latent_score_kernel<T, 8, 1>; break;
+    case 161: k = latent_score_kernel<T, 16, 1>; break;
+    case 321: k = latent_score_kernel<T, 32, 1>; break;
+    case 322: k = latent_score_kernel<T, 32, 2>; break;
+    case 324: k = latent_score_kernel<T, 32, 4>; break;
+    default: return fail(SALS_ERR_UNSUPPORTED, "score rank layout");
+  }
+  SALS_CUDA_TRY(launch(k, grid, dim3(256), 0, st, 1, a));
+  return SALS_OK;
+}
+
+sals_status launch_topk(const TopkArgs& a, int batch, int cs, size_t smem, cudaStream_t st) {
+  static bool attr_done = false;
+  if (!attr_done) {
+    SALS_CUDA_TRY(cudaFuncSetAttribute(topk_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    SALS_CUDA_TRY(cudaFuncSetAttribute(topk_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr_done = true;
+  }
+  SALS_CUDA_TRY(launch(topk_cluster_kernel, dim3(batch * cs), dim3(512), smem, st, cs, a));
+  return SALS_OK;
+}
+
+template <typename T>
+sals_status launch_recon_simt(const sals_config* c, ReconArgs a, int batch, int kmax, cudaStream_t st) {
+  const int DH = c->head_dim;
+  const size_t smem = (size_t)(32 * 33 + DH * 33 + 32 * DH) * 4;
+  static bool attr_done = false;
+  if (!attr_done) {
+    SALS_CUDA_TRY(cudaFuncSetAttribute(recon_rope_simt_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+    attr_done = true;
+  }
+  dim3 grid(ceil_div(kmax, 32), c->num_kv_heads, batch);
+  SALS_CUDA_TRY(launch(recon_rope_simt_kernel<T>, grid, dim3(256), smem, st, 1, a));
+  return SALS_OK;
+}
+
+template <typename T, bool DENSE>
+sals_status launch_flash(const sals_config* c, FlashArgs a, int batch, cudaStream_t st) {
+  const int G = c->num_q_heads / c->num_kv_heads;
+  void (*k)(FlashArgs) = nullptr;
+#define SALS_FD_CASE(DH)                                                     \
+  case DH:                                                                   \
+    switch (G) {                                                             \
+      case 1: k = flash_decode_kernel<T, DH, 1, DENSE>; break;               \
+      case 2: k = flash_decode_kernel<T, DH, 2, DENSE>; break;               \
+      case 4: k = flash_decode_kernel<T, DH, 4, DENSE>; break;               \
+      case 8: k = flash_decode_kernel<T, DH, 8, DENSE>; break;               \
+    }                                                                        \
+    break;
+  if (sizeof(T) == 2) {
+    switch (c->head_dim) { SALS_FD_CASE(16) SALS_FD_CASE(32) SALS_FD_CASE(64) SALS_FD_CASE(128) SALS_FD_CASE(256) }
+  } else {
+    switch (c->head_dim) { SALS_FD_CASE(16) SALS_FD_CASE(32) SALS_FD_CASE(64) SALS_FD_CASE(128) }
+  }
+#undef SALS_FD_CASE
+  if (!k) return fail(SALS_ERR_UNSUPPORTED, "flash decode shape");
+  dim3 grid(ceil_div(a.nsplit, 4), c->num_kv_heads, batch);
+  SALS_CUDA_TRY(launch(k, grid, dim3(128), 0, st, 1, a));
+  return SALS_OK;
+}
+
+template <typename T>
+sals_status launch_merge(const sals_config* c, MergeArgs a, int batch, cudaStream_t st) {
+  SALS_CUDA_TRY(launch(merge_kernel<T>, dim3(batch * c->num_q_heads), dim3(std::max(32, c->head_dim)), 0, st, 1, a));
+  return SALS_OK;
+}
+
+// Shared tail of decode: reconstruct + RoPE + attention + merge over a token
+// list sel/count (local rows), producing either y (T) or one fp32 partial per
+// (b, h) when `partial_out` is set.
+template <typename T>
+sals_status attend_list(const sals_config* c, const Plan& p, const void* U, const void* latent,
+                        const void* v_cache, int64_t cap, int batch, int64_t pos_base, const int* sel,
+                        const int* count, char* ws, void* out, float* partial_out, cudaStream_t st) {
+  float* part = reinterpret_cast<float*>(ws + p.off_part);
+  const float* qrope = reinterpret_cast<const float*>(ws + p.off_qrope);
+  if (p.tc) {
+    TcArgs t{};
+    t.latent = latent; t.cap = cap; t.r = c->rank; t.U = U; t.v_cache = v_cache;
+    t.sel = sel; t.count = count; t.k_stride = c->top_k; t.D = p.D; t.head_dim = c->head_dim;
+    t.G = p.G; t.n_q = c->num_q_heads; t.pos_base = pos_base; t.rope = make_rope(c);
+    t.qrope = qrope; t.scale_log2 = scale_log2(c); t.partials = part; t.ntiles = p.nsplit;
+    sals_status s = launch_recon_attn_tc(t, batch, st);
+    if (s != SALS_OK) return fail(s, "%s", tc_last_error());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  } else {
+    ReconArgs r{};
+    r.latent = latent; r.cap = cap; r.r = c->rank; r.U = U; r.sel = sel; r.count = count;
+    r.k_stride = c->top_k; r.D = p.D; r.head_dim = c->head_dim; r.pos_base = pos_base;
+    r.rope = make_rope(c); r.kr = ws + p.off_kr;
+    sals_status s = launch_recon_simt<T>(c, r, batch, p.kmax, st);
+    if (s != SALS_OK) return s;
+    FlashArgs f{};
+    f.qrope = qrope; f.kbase = ws + p.off_kr; f.v_cache = v_cache; f.sel = sel; f.count = count;
+    f.cap = cap; f.D = p.D; f.k_stride = c->top_k; f.n_q = c->num_q_heads; f.n_kv = c->num_kv_heads;
+    f.nsplit = p.nsplit; f.chunk = p.chunk; f.scale_log2 = scale_log2(c); f.partials = part;
+    s = launch_flash<T, false>(c, f, batch, st);
+    if (s != SALS_OK) return s;
+  }
+  MergeArgs m{};
+  m.partials = part;
+  m.bh_stride = (int64_t)p.nsplit * (c->head_dim + 2);
+  m.s_stride = c->head_dim + 2;
+  m.nsplit = p.nsplit; m.n_q = c->num_q_heads; m.head_dim = c->head_dim;
+  m.out = partial_out ? (void*)partial_out : out;
+  m.normalize = partial_out ? 0 : 1;
+  if (partial_out) return launch_merge<float>(c, m, batch, st);
+  return launch_merge<T>(c, m, batch, st);
+}
+
+template <typename T>
+sals_status decode_impl(const sals_config* c, const void* U, const void* q, const void* latent,
+                        const void* v_cache, int64_t cap, int batch, const int* seq_len, int max_s,
+                        void* out, int* sel_out, float* scores_out, char* ws, const Plan& p,
+                        cudaStream_t st) {
+  float* qtil = reinterpret_cast<float*>(ws + p.off_qtil);
+  float* qrope = reinterpret_cast<float*>(ws + p.off_qrope);
+  int* sel = reinterpret_cast<int*>(ws + p.off_sel);
+  int* count = reinterpret_cast<int*>(ws + p.off_count);
+  float* scores = scores_out ? scores_out : reinterpret_cast<float*>(ws + p.off_scores);
+  const int64_t sstride = scores_out ? max_s : p.score_stride;
+
+  ProjectArgs pa{};
+  pa.U = U; pa.x = q; pa.x_stride = c->num_q_heads * c->head_dim; pa.D = p.D; pa.r = c->rank;
+  pa.ncols = c->score_rank; pa.B = batch; pa.head_dim = c->head_dim; pa.group = p.G;
+  pa.n_q = c->num_q_heads; pa.out_f32 = qtil; pa.qrope = qrope; pa.seq_len = seq_len; pa.rope = make_rope(c);
+  sals_status s = launch_project<T>(c, p, true, pa, c->score_rank, st);
+  if (s != SALS_OK) return s;
+
+  ScoreArgs sa{};
+  sa.latent = latent; sa.cap = cap; sa.r = c->rank; sa.rstar = c->score_rank; sa.qtil = qtil;
+  sa.len = seq_len; sa.scores = scores; sa.stride = sstride;
+  s = launch_score<T>(c, sa, batch, max_s, st);
+  if (s != SALS_OK) return s;
+
+  TopkArgs ta{};
+  ta.scores = scores; ta.score_stride = sstride; ta.seq_len = seq_len; ta.idx_base = 0;
+  ta.k = c->top_k; ta.sink = c->sink; ta.recent = c->recent; ta.mode = 0; ta.slice = p.tk_slice;
+  ta.sel_out = sel; ta.sel_stride = c->top_k; ta.sel_count = count; ta.pad_to = c->top_k;
+  ta.sel_out2 = sel_out;
+  s = launch_topk(ta, batch, p.tk_cs, p.tk_smem, st);
+  if (s != SALS_OK) return s;
+
+  return attend_list<T>(c, p, U, latent, v_cache, cap, batch, 0, sel, count, ws, out, nullptr, st);
+}
+
+}  // namespace
+
+// =====================================================================  C ABI
+extern "C" {
+
+const char* sals_status_string(sals_status s) {
+  switch (s) {
+    case SALS_OK: return "SALS_OK";
+    case SALS_ERR_INVALID_ARGUMENT: return "SALS_ERR_INVALID_ARGUMENT";
+    case SALS_ERR_UNSUPPORTED: return "SALS_ERR_UNSUPPORTED";
+    case SALS_ERR_WORKSPACE_TOO_SMALL: return "SALS_ERR_WORKSPACE_TOO_SMALL";
+    case SALS_ERR_CUDA: return "SALS_ERR_CUDA";
+  }
+  return "SALS_ERR_UNKNOWN";
+}
+
+const char* sals_last_error(void) { return g_err.c_str(); }
+
+uint64_t sals_launch_count(int32_t reset) {
+  return reset ? g_launches.exchange(0) : g_launches.load();
+}
+
+size_t sals_workspace_bytes(const sals_config* cfg, int32_t batch, int32_t max_seq_len) {
+  if (validate(cfg) != SALS_OK || batch < 1 || max_seq_len < 1) return 0;
+  Plan p{};
+  if (make_plan(cfg, batch, max_seq_len, p, true) != SALS_OK) return 0;
+  return p.total;
+}
+
+sals_status sals_append_latent(const sals_config* cfg, const void* U, const void* k_new, const void* v_new,
+                               int32_t batch, const int32_t* d_pos, void* latent_cache, void* v_cache,
+                               int64_t cap, void* stream) {
+  sals_status s = validate(cfg);
+  if (s != SALS_OK) return s;
+  if (!U || !k_new || !v_new || !d_pos || !latent_cache || !v_cache)
+    return fail(SALS_ERR_INVALID_ARGUMENT, "NULL tensor argument");
+  if (batch < 1 || batch > 65535 || cap < 1) return fail(SALS_ERR_INVALID_ARGUMENT, "bad batch / cap");
+  Plan p{};
+  p.D = cfg->num_kv_heads * cfg->head_dim;
+  p.proj_cs = std::min(16, std::max(1, ceil_div(p.D, 64)));
+  p.proj_rows = ceil_div(p.D, p.proj_cs);
+  ProjectArgs a{};
+  a.U = U; a.x = k_new; a.x_stride = p.D; a.D = p.D; a.r = cfg->rank; a.ncols = cfg->rank; a.B = batch;
+  a.head_dim = cfg->head_dim; a.group = 1; a.n_q = cfg->num_q_heads; a.latent = latent_cache; a.cap = cap;
+  a.pos = d_pos; a.v_new = v_new; a.v_cache = v_cache;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (cfg->dtype == SALS_BF16) return launch_project<__nv_bfloat16>(cfg, p, false, a, cfg->rank, st);
+  return launch_project<float>(cfg, p, false, a, cfg->rank, st);
+}
+
+sals_status sals_decode(const sals_config* cfg, const void* U, const void* q, const void* latent_cache,
+                        const void* v_cache, int64_t cap, int32_t batch, const int32_t* d_seq_len,
+                        int32_t max_seq_len, void* out, int32_t* sel_idx_out, float* scores_out,
+                        void* workspace, size_t ws_bytes, void* stream) {
+  sals_status s = validate(cfg);
+  if (s != SALS_OK) return s;
+  if (!U || !q || !latent_cache || !v_cache || !d_seq_len || !out || !workspace)
+    return fail(SALS_ERR_INVALID_ARGUMENT, "NULL tensor argument");
+  if (batch < 1 || batch > 65535) return fail(SALS_ERR_UNSUPPORTED, "batch %d outside [1, 65535]", batch);
+  if (max_seq_len < 1 || max_seq_len > cap) return fail(SALS_ERR_INVALID_ARGUMENT, "need 1 <= max_seq_len <= cap");
+  if (max_seq_len > 524288) return fail(SALS_ERR_UNSUPPORTED, "max_seq_len > 524288");
+  if (reinterpret_cast<uintptr_t>(workspace) % 256) return fail(SALS_ERR_INVALID_ARGUMENT, "workspace not 256-B aligned");
+  Plan p{};
+  s = make_plan(cfg, batch, max_seq_len, p, false);
+  if (s != SALS_OK) return s;
+  if (ws_bytes < p.total) return fail(SALS_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu", ws_bytes, p.total);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  char* ws = reinterpret_cast<char*>(workspace);
+  if (cfg->dtype == SALS_BF16)
+    return decode_impl<__nv_bfloat16>(cfg, U, q, latent_cache, v_cache, cap, batch, d_seq_len, max_seq_len, out,
+                                      sel_idx_out, scores_out, ws, p, st);
+  return decode_impl<float>(cfg, U, q, latent_cache, v_cache, cap, batch, d_seq_len, max_seq_len, out,
+                            sel_idx_out, scores_out, ws, p, st);
+}
+
+// ------------------------------------------------------------ dense baseline
+size_t sals_dense_workspace_bytes(const sals_config* cfg, int32_t batch, int32_t max_seq_len) {
+  if (validate(cfg) != SALS_OK || batch < 1 || max_seq_len < 1) return 0;
+  int nsplit, chunk;
+  plan_flash(batch, cfg->num_kv_heads, max_seq_len, flash_tpw_unr(cfg), nsplit, chunk);
+  return align_up((size_t)batch * cfg->num_q_heads * cfg->head_dim * 4, 256) +
+         align_up((size_t)batch * cfg->num_q_heads * nsplit * (cfg->head_dim + 2) * 4, 256);
+}
+
+sals_status sals_dense_append(const sals_config* cfg, const void* k_new, const void* v_new, int32_t batch,
+                              const int32_t* d_pos, void* k_cache, void* v_cache, int64_t cap, void* stream) {
+  sals_status s = validate(cfg);
+  if (s != SALS_OK) return s;
+  if (!k_new || !v_new || !d_pos || !k_cache || !v_cache) return fail(SALS_ERR_INVALID_ARGUMENT, "NULL tensor argument");
+  if (batch < 1 || batch > 65535) return fail(SALS_ERR_INVALID_ARGUMENT, "bad batch");
+  DenseAppendArgs a{};
+  a.k_new = k_new; a.v_new = v_new; a.pos = d_pos; a.k_cache = k_cache; a.v_cache = v_cache; a.cap = cap;
+  a.D = cfg->num_kv_heads * cfg->head_dim; a.head_dim = cfg->head_dim; a.n_kv = cfg->num_kv_heads;
+  a.rope = make_rope(cfg);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (cfg->dtype == SALS_BF16) SALS_CUDA_TRY(launch(dense_append_kernel<__nv_bfloat16>, dim3(batch), dim3(256), 0, st, 1, a));
+  else SALS_CUDA_TRY(launch(dense_append_kernel<float>, dim3(batch), dim3(256), 0, st, 1, a));
+  return SALS_OK;
+}
+
+sals_status sals_dense_decode(const sals_config* cfg, const void* q, const void* k_cache, const void* v_cache,
+                              int64_t cap, int32_t batch, const int32_t* d_seq_len, int32_t max_seq_len,
+                              void* out, void* workspace, size_t ws_bytes, void* stream) {
+  sals_status s = validate(cfg);
+  if (s != SALS_OK) return s;
+  if (!q || !k_cache || !v_cache || !d_seq_len || !out || !workspace)
+    return fail(SALS_ERR_INVALID_ARGUMENT, "NULL tensor argument");
+  if (batch < 1 || batch > 65535 || max_seq_len < 1 || max_seq_len > cap)
+    return fail(SALS_ERR_INVALID_ARGUMENT, "bad batch / max_seq_len");
+  if (ws_bytes < sals_dense_workspace_bytes(cfg, batch, max_seq_len))
+    return fail(SALS_ERR_WORKSPACE_TOO_SMALL, "dense workspace too small");
+  int nsplit, chunk;
+  plan_flash(batch, cfg->num_kv_heads, max_seq_len, flash_tpw_unr(cfg), nsplit, chunk);
+  char* ws = reinterpret_cast<char*>(workspace);
+  float* qrope = reinterpret_cast<float*>(ws);
+  float* part = reinterpret_cast<float*>(ws + align_up((size_t)batch * cfg->num_q_heads * cfg->head_dim * 4, 256));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Plan p{};
+  p.D = cfg->num_kv_heads * cfg->head_dim;
+  p.G = cfg->num_q_heads / cfg->num_kv_heads;
+  p.proj_cs = 1;
+  p.proj_rows = std::min(p.D, 512);
+  // query RoPE via the projection kernel's second role (no projection columns)
+  ProjectArgs pa{};
+  pa.x = q; pa.x_stride = cfg->num_q_heads * cfg->head_dim; pa.B = batch; pa.n_q = cfg->num_q_heads;
+  pa.head_dim = cfg->head_dim; pa.qrope = qrope; pa.seq_len = d_seq_len; pa.rope = make_rope(cfg);
+  FlashArgs f{};
+  f.qrope = qrope; f.kbase = k_cache; f.v_cache = v_cache; f.count = d_seq_len; f.cap = cap; f.D = p.D;
+  f.k_stride = 0; f.n_q = cfg->num_q_heads; f.n_kv = cfg->num_kv_heads; f.nsplit = nsplit; f.chunk = chunk;
+  f.scale_log2 = scale_log2(cfg); f.partials = part;
+  MergeArgs m{};
+  m.partials = part; m.bh_stride = (int64_t)nsplit * (cfg->head_dim + 2); m.s_stride = cfg->head_dim + 2;
+  m.nsplit = nsplit; m.n_q = cfg->num_q_heads; m.head_dim = cfg->head_dim; m.out = out; m.normalize = 1;
+  if (cfg->dtype == SALS_BF16) {
+    SALS_CUDA_TRY(launch(project_kernel<__nv_bfloat16, true>, dim3(1, 1), dim3(128), 0, st, 1, pa));
+    s = launch_flash<__nv_bfloat16, true>(cfg, f, batch, st);
+    if (s != SALS_OK) return s;
+    return launch_merge<__nv_bfloat16>(cfg, m, batch, st);
+  }
+  SALS_CUDA_TRY(launch(project_kernel<float, true>, dim3(1, 1), dim3(128), 0, st, 1, pa));
+  s = launch_flash<float, true>(cfg, f, batch, st);
+  if (s != SALS_OK) return s;
+  return launch_merge<float>(cfg, m, batch, st);
+}
+
+// ------------------------------------------------------------ sharded decode
+size_t sals_shard_workspace_bytes(const sals_config* cfg, int32_t batch, int32_t max_local_len, int32_t world) {
+  if (validate(cfg) != SALS_OK || batch < 1 || max_local_len < 1 || world < 1) return 0;
+  Plan p{};
+  if (make_plan(cfg, batch, std::max(max_local_len, 1), p, true) != SALS_OK) return 0;
+  // extra: global selection [B, k] + count
+  return align_up(p.total, 256) + align_up((size_t)batch * cfg->top_k * 4, 256) + align_up((size_t)batch * 4, 256);
+}
+
+sals_status sals_shard_candidates(const sals_config* cfg, const void* U, const void* q, const void* latent_shard,
+                                  int64_t cap_local, int32_t batch, int64_t shard_start,
+                                  const int32_t* d_local_len, int32_t max_local_len, const int32_t* d_seq_len,
+                                  float* cand_score, int32_t* cand_idx, void* workspace, size_t ws_bytes,
+                                  void* stream) {
+  sals_status s = validate(cfg);
+  if (s != SALS_OK) return s;
+  if (!U || !q || !latent_shard || !d_local_len || !d_seq_len || !cand_score || !cand_idx || !workspace)
+    return fail(SALS_ERR_INVALID_ARGUMENT, "NULL tensor argument");
+  if (batch < 1 || max_local_len < 1 || max_local_len > cap_local || shard_start < 0)
+    return fail(SALS_ERR_INVALID_ARGUMENT, "bad shard geometry");
+  Plan p{};
+  s = make_plan(cfg, batch, max_local_len, p, false);
+  if (s != SALS_OK) return s;
+  if (ws_bytes < sals_shard_workspace_bytes(cfg, batch, max_local_len, 1))
+    return fail(SALS_ERR_WORKSPACE_TOO_SMALL, "shard workspace too small");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  char* ws = reinterpret_cast<char*>(workspace);
+  float* qtil = reinterpret_cast<float*>(ws + p.off_qtil);
+  float* scores = reinterpret_cast<float*>(ws + p.off_scores);
+  ProjectArgs pa{};
+  pa.U = U; pa.x = q; pa.x_stride = cfg->num_q_heads * cfg->head_dim; pa.D = p.D; pa.r = cfg->rank;
+  pa.ncols = cfg->score_rank; pa.B = batch; pa.head_dim = cfg->head_dim; pa.group = p.G; pa.n_q = cfg->num_q_heads;
+  pa.out_f32 = qtil; pa.qrope = reinterpret_cast<float*>(ws + p.off_qrope); pa.seq_len = d_seq_len;
+  pa.rope = make_rope(cfg);
+  ScoreArgs sa{};
+  sa.latent = latent_shard; sa.cap = cap_local; sa.r = cfg->rank; sa.rstar = cfg->score_rank; sa.qtil = qtil;
+  sa.len = d_local_len; sa.scores = scores; sa.stride = p.score_stride;
+  if (cfg->dtype == SALS_BF16) {
+    s = launch_project<__nv_bfloat16>(cfg, p, true, pa, cfg->score_rank, st);
+    if (s == SALS_OK) s = launch_score<__nv_bfloat16>(cfg, sa, batch, max_local_len, st);
+  } else {
+    s = launch_project<float>(cfg, p, true, pa, cfg->score_rank, st);
+    if (s == SALS_OK) s = launch_score<float>(cfg, sa, batch, max_local_len, st);
+  }
+  if (s != SALS_OK) return s;
+  TopkArgs ta{};
+  ta.scores = scores; ta.score_stride = p.score_stride; ta.n_entries = d_local_len; ta.seq_len = d_seq_len;
+  ta.idx_base = shard_start; ta.k = cfg->top_k; ta.sink = cfg->sink; ta.recent = cfg->recent; ta.mode = 1;
+  ta.slice = p.tk_slice; ta.sel_out = cand_idx; ta.sel_stride = cfg->top_k; ta.sel_score = cand_score;
+  ta.pad_to = cfg->top_k;
+  return launch_topk(ta, batch, p.tk_cs, p.tk_smem, st);
+}
+
+sals_status sals_shard_attend(const sals_config* cfg, const void* U, const void* q, const void* latent_shard,
+                              const void* v_shard, int64_t cap_local, int32_t batch, int64_t shard_start,
+                              const int32_t* d_local_len, int32_t max_local_len, const int32_t* d_seq_len,
+                              const float* cand_all_score, const int32_t* cand_all_idx, int32_t world,
+                              float* partial, void* workspace, size_t ws_bytes, void* stream) {
+  sals_status s = validate(cfg);
+  if (s != SALS_OK) return s;
+  if (!U || !q || !latent_shard || !v_shard || !d_local_len || !d_seq_len || !cand_all_score || !cand_all_idx ||
+      !partial || !workspace)
+    return fail(SALS_ERR_INVALID_ARGUMENT, "NULL tensor argument");
+  if (world < 1 || batch < 1 || max_local_len < 1 || max_local_len > cap_local)
+    return fail(SALS_ERR_INVALID_ARGUMENT, "bad shard geometry");
+  Plan p{};
+  s = make_plan(cfg, batch, max_local_len, p, false);
+  if (s != SALS_OK) return s;
+  if (ws_bytes < sals_shard_workspace_bytes(cfg, batch, max_local_len, world))
+    return fail(SALS_ERR_WORKSPACE_TOO_SMALL, "shard workspace too small");
+  // top-k over the gathered candidates: its own cluster plan
+  Plan pk{};
+  s = plan_topk(world * cfg->top_k, true, pk);
+  if (s != SALS_OK) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  char* ws = reinterpret_cast<char*>(workspace);
+  int* gsel = reinterpret_cast<int*>(ws + align_up(p.total, 256));
+  int* gcount = reinterpret_cast<int*>(ws + align_up(p.total, 256) + align_up((size_t)batch * cfg->top_k * 4, 256));
+  int* own = reinterpret_cast<int*>(ws + p.off_sel);
+  int* own_count = reinterpret_cast<int*>(ws + p.off_count);
+  TopkArgs ta{};
+  ta.scores = cand_all_score; ta.cand_idx = cand_all_idx; ta.n_const = world * cfg->top_k;
+  ta.seg_len = cfg->top_k; ta.seg_stride = (int64_t)batch * cfg->top_k; ta.seq_len = d_seq_len;
+  ta.k = cfg->top_k; ta.sink = cfg->sink; ta.recent = cfg->recent; ta.mode = 1; ta.slice = pk.tk_slice;
+  ta.sel_out = gsel; ta.sel_stride = cfg->top_k; ta.sel_count = gcount; ta.pad_to = cfg->top_k;
+  s = launch_topk(ta, batch, pk.tk_cs, pk.tk_smem, st);
+  if (s != SALS_OK) return s;
+  OwnedArgs oa{};
+  oa.gsel = gsel; oa.gcount = gcount; oa.g_stride = cfg->top_k; oa.seq_len = d_seq_len; oa.local_len = d_local_len;
+  oa.shard_start = shard_start; oa.sink = cfg->sink; oa.recent = cfg->recent; oa.k = cfg->top_k;
+  oa.own_sel = own; oa.own_count = own_count;
+  SALS_CUDA_TRY(launch(owned_list_kernel, dim3(batch), dim3(256), 0, st, 1, oa));
+  if (cfg->dtype == SALS_BF16)
+    return attend_list<__nv_bfloat16>(cfg, p, U, latent_shard, v_shard, cap_local, batch, shard_start, own,
+                                      own_count, ws, nullptr, partial, st);
+  return attend_list<float>(cfg, p, U, latent_shard, v_shard, cap_local, batch, shard_start, own, own_count, ws,
+                            nullptr, partial, st);
+}
+
+sals_status sals_merge_partials(const sals_config* cfg, const float* partial_all, int32_t world, int32_t batch,
+                                void* out, void* stream) {
+  sals_status s = validate(cfg);
+  if (s != SALS_OK) return s;
+  if (!partial_all || !out || world < 1 || batch < 1) return fail(SALS_ERR_INVALID_ARGUMENT, "bad merge arguments");
+  MergeArgs m{};
+  m.partials = partial_all; m.bh_stride = cfg->head_dim + 2;
+  m.s_stride = (int64_t)batch * cfg->num_q_heads * (cfg->head_dim + 2);
+  m.nsplit = world; m.n_q = cfg->num_q_heads; m.head_dim = cfg->head_dim; m.out = out; m.normalize = 1;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (cfg->dtype == SALS_BF16) return launch_merge<__nv_bfloat16>(cfg, m, batch, st);
+  return launch_merge<float>(cfg, m, batch, st);
+}
+
+}  // extern "C"

@@ -1,0 +1,333 @@
+// SIMT kernels of the reconstruction / attention stages (path S) and of the
+// dense comparator:
+//   recon_rope_simt_kernel  K_C = K~_C U^T then K^R_C = RoPE_j(K_C)   (Alg. 1 lines 6-7)
+//   flash_decode_kernel     split-K online-softmax attention over a token list
+//                           (Alg. 1 lines 8-9 / Eq. 6; also the dense flash decode)
+//   merge_kernel            log-sum-exp merge of the split partials -> y
+//   dense_append_kernel     post-RoPE dense cache write (comparator)
+//   owned_list_kernel       sharded: local rows a rank attends to
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sals {
+
+// ---------------------------------------------------------------------------
+// Reconstruct + RoPE, one (32-row tile, KV head) per CTA.  fp32 FMA GEMM with
+// shared-memory tiles; the rows of A are gathered latent rows.
+// ---------------------------------------------------------------------------
+constexpr int kRcRows = 32, kRcK = 32, kRcThreads = 256;
+
+template <typename T>
+__global__ void __launch_bounds__(kRcThreads)
+recon_rope_simt_kernel(ReconArgs a) {
+  extern __shared__ float rc_smem[];
+  const int DH = a.head_dim;
+  float* As = rc_smem;                          // [32][33]
+  float* Bs = As + kRcRows * (kRcK + 1);        // [DH][33]
+  float* Ks = Bs + DH * (kRcK + 1);             // [32][DH]
+  __shared__ int rows[kRcRows];
+  const int b = blockIdx.z, g = blockIdx.y, t0 = blockIdx.x * kRcRows;
+  const int tid = threadIdx.x;
+  const T* lat = reinterpret_cast<const T*>(a.latent);
+  const T* U = reinterpret_cast<const T*>(a.U);
+
+  pdl_wait();
+  const int cnt = a.count[b];
+  if (t0 >= cnt) { pdl_launch_dependents(); return; }
+  if (tid < kRcRows) rows[tid] = (t0 + tid < cnt) ? a.sel[(size_t)b * a.k_stride + t0 + tid] : -1;
+  __syncthreads();
+
+  const int nout = kRcRows * DH / kRcThreads;   // outputs per thread (DH >= 8)
+  float acc[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+
+  for (int k0 = 0; k0 < a.r; k0 += kRcK) {
+    for (int i = tid; i < kRcRows * kRcK; i += kRcThreads) {
+      const int rr = i / kRcK, kk = i % kRcK;
+      const int row = rows[rr];
+      As[rr * (kRcK + 1) + kk] = (row >= 0 && k0 + kk < a.r)
+          ? Elem<T>::to_f(lat[((size_t)b * a.cap + row) * a.r + k0 + kk]) : 0.f;
+    }
+    for (int i = tid; i < DH * kRcK; i += kRcThreads) {
+      const int nn = i / kRcK, kk = i % kRcK;
+      Bs[nn * (kRcK + 1) + kk] = (k0 + kk < a.r) ? Elem<T>::to_f(U[(size_t)(g * DH + nn) * a.r + k0 + kk]) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (j < nout) {
+        const int o = tid + j * kRcThreads, rr = o / DH, nn = o % DH;
+        float s = acc[j];
+#pragma unroll 8
+        for (int kk = 0; kk < kRcK; ++kk) s = fmaf(As[rr * (kRcK + 1) + kk], Bs[nn * (kRcK + 1) + kk], s);
+        acc[j] = s;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    if (j < nout) Ks[tid + j * kRcThreads] = acc[j];
+  __syncthreads();
+  // RoPE at the original position of each row, then store K^R_C
+  const int half = DH / 2;
+  T* kr = reinterpret_cast<T*>(a.kr);
+  for (int i = tid; i < kRcRows * half; i += kRcThreads) {
+    const int rr = i / half, p = i % half;
+    const int row = rows[rr];
+    if (row < 0) continue;
+    int lo, hi; rope_pair(p, half, a.rope.style, lo, hi);
+    float c, s; rope_cs(a.rope.theta[p], a.pos_base + row, c, s);
+    const float xl = Ks[rr * DH + lo], xh = Ks[rr * DH + hi];
+    T* dst = kr + ((size_t)b * a.k_stride + t0 + rr) * a.D + g * DH;
+    dst[lo] = Elem<T>::from_f(xl * c - xh * s);
+    dst[hi] = Elem<T>::from_f(xl * s + xh * c);
+  }
+  pdl_launch_dependents();
+}
+
+template __global__ void recon_rope_simt_kernel<float>(ReconArgs);
+template __global__ void recon_rope_simt_kernel<__nv_bfloat16>(ReconArgs);
+
+// ---------------------------------------------------------------------------
+// Flash decode over a token list.  One warp per (request, KV head, split);
+// LPT lanes cover one token row of one head with 16-byte loads, TPW tokens per
+// warp step.  Each lane holds the rotated query of all G heads of the group
+// for its EPL dims (so a K/V row load serves G query heads, GQA-aware).
+// Logits are in the log2 domain (q pre-scaled by scale * log2 e).
+// ---------------------------------------------------------------------------
+constexpr int kFdWarps = 4;
+
+template <typename T, int DH, int G, bool DENSE>
+__global__ void __launch_bounds__(kFdWarps * 32)
+flash_decode_kernel(FlashArgs a) {
+  constexpr int EPL = Elem<T>::kPer16;
+  constexpr int LPT = DH / EPL;            // lanes per token row
+  static_assert(LPT >= 1 && LPT <= 32, "head row must fit one warp");
+  constexpr int TPW = 32 / LPT;            // tokens per warp step
+  constexpr int UNR = 2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = lane / LPT, li = lane % LPT;
+  const int b = blockIdx.z, g = blockIdx.y;
+  const int split = blockIdx.x * kFdWarps + warp;
+
+  pdl_wait();
+  if (split >= a.nsplit) return;
+  const int cnt = a.count[b];
+  const int t0 = split * a.chunk;
+  const int t1 = min(cnt, t0 + a.chunk);
+
+  float q[G][EPL];
+#pragma unroll
+  for (int h = 0; h < G; ++h)
+#pragma unroll
+    for (int e = 0; e < EPL; ++e)
+      q[h][e] = a.qrope[((size_t)b * a.n_q + g * G + h) * DH + li * EPL + e] * a.scale_log2;
+  float m[G], l[G], o[G][EPL];
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+    m[h] = -INFINITY; l[h] = 0.f;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) o[h][e] = 0.f;
+  }
+  const char* kb = reinterpret_cast<const char*>(a.kbase);
+  const char* vb = reinterpret_cast<const char*>(a.v_cache);
+  const size_t rowb = (size_t)a.D * sizeof(T);
+  const size_t headoff = (size_t)g * DH * sizeof(T) + li * 16;
+
+  for (int tb = t0; tb < t1; tb += TPW * UNR) {
+    uint4 kr[UNR], vr[UNR];
+    bool ok[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int t = tb + u * TPW + sub;
+      ok[u] = t < t1;
+      if (ok[u]) {
+        size_t krow, vrow;
+        if (DENSE) {
+          krow = vrow = (size_t)b * a.cap + t;
+        } else {
+          krow = (size_t)b * a.k_stride + t;
+          vrow = (size_t)b * a.cap + a.sel[(size_t)b * a.k_stride + t];
+        }
+        kr[u] = ld_nc_v4(kb + krow * rowb + headoff);
+        vr[u] = ld_nc_v4(vb + vrow * rowb + headoff);
+      } else {
+        kr[u] = vr[u] = make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      float kf[EPL], vf[EPL];
+      Elem<T>::unpack(kr[u], kf);
+      Elem<T>::unpack(vr[u], vf);
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        float s = 0.f;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) s = fmaf(q[h][e], kf[e], s);
+#pragma unroll
+        for (int off = LPT / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (ok[u]) {
+          const float mn = fmaxf(m[h], s);
+          const float corr = exp2f(m[h] - mn);      // m = -inf -> 0
+          const float p = exp2f(s - mn);
+          l[h] = l[h] * corr + p;
+#pragma unroll
+          for (int e = 0; e < EPL; ++e) o[h][e] = fmaf(p, vf[e], o[h][e] * corr);
+          m[h] = mn;
+        }
+      }
+    }
+  }
+  // merge the TPW token groups of the warp
+#pragma unroll
+  for (int off = LPT; off < 32; off <<= 1) {
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      const float mo = __shfl_xor_sync(0xffffffffu, m[h], off);
+      const float lo = __shfl_xor_sync(0xffffffffu, l[h], off);
+      const float mn = fmaxf(m[h], mo);
+      const float c1 = (m[h] == -INFINITY) ? 0.f : exp2f(m[h] - mn);
+      const float c2 = (mo == -INFINITY) ? 0.f : exp2f(mo - mn);
+      l[h] = l[h] * c1 + lo * c2;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        const float oo = __shfl_xor_sync(0xffffffffu, o[h][e], off);
+        o[h][e] = o[h][e] * c1 + oo * c2;
+      }
+      m[h] = mn;
+    }
+  }
+  if (sub == 0) {
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      float* dst = a.partials + (((size_t)b * a.n_q + g * G + h) * a.nsplit + split) * (DH + 2);
+      if (li == 0) { dst[0] = m[h]; dst[1] = l[h]; }
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) dst[2 + li * EPL + e] = o[h][e];
+    }
+  }
+  pdl_launch_dependents();
+}
+
+#define SALS_FD_INST(T, DH)                                                  \
+  template __global__ void flash_decode_kernel<T, DH, 1, false>(FlashArgs);  \
+  template __global__ void flash_decode_kernel<T, DH, 2, false>(FlashArgs);  \
+  template __global__ void flash_decode_kernel<T, DH, 4, false>(FlashArgs);  \
+  template __global__ void flash_decode_kernel<T, DH, 8, false>(FlashArgs);  \
+  template __global__ void flash_decode_kernel<T, DH, 1, true>(FlashArgs);   \
+  template __global__ void flash_decode_kernel<T, DH, 2, true>(FlashArgs);   \
+  template __global__ void flash_decode_kernel<T, DH, 4, true>(FlashArgs);   \
+  template __global__ void flash_decode_kernel<T, DH, 8, true>(FlashArgs);
+SALS_FD_INST(float, 16)
+SALS_FD_INST(float, 32)
+SALS_FD_INST(float, 64)
+SALS_FD_INST(float, 128)
+SALS_FD_INST(__nv_bfloat16, 16)
+SALS_FD_INST(__nv_bfloat16, 32)
+SALS_FD_INST(__nv_bfloat16, 64)
+SALS_FD_INST(__nv_bfloat16, 128)
+SALS_FD_INST(__nv_bfloat16, 256)
+
+// ---------------------------------------------------------------------------
+// LSE merge: y_h = sum_s o_s 2^(m_s - M) / sum_s l_s 2^(m_s - M)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void merge_kernel(MergeArgs a) {
+  const int bh = blockIdx.x;
+  const int b = bh / a.n_q, h = bh % a.n_q;
+  pdl_wait();
+  const float* base = a.partials + (size_t)bh * a.bh_stride;
+  float M = -INFINITY;
+  for (int s = 0; s < a.nsplit; ++s) M = fmaxf(M, base[(size_t)s * a.s_stride]);
+  float L = 0.f;
+  for (int s = 0; s < a.nsplit; ++s) {
+    const float ms = base[(size_t)s * a.s_stride];
+    if (ms != -INFINITY) L += base[(size_t)s * a.s_stride + 1] * exp2f(ms - M);
+  }
+  const float invL = (L > 0.f) ? 1.f / L : 0.f;
+  for (int i = threadIdx.x; i < a.head_dim; i += blockDim.x) {
+    float acc = 0.f;
+    for (int s = 0; s < a.nsplit; ++s) {
+      const float ms = base[(size_t)s * a.s_stride];
+      if (ms != -INFINITY) acc += base[(size_t)s * a.s_stride + 2 + i] * exp2f(ms - M);
+    }
+    if (a.normalize) {
+      T* out = reinterpret_cast<T*>(a.out) + ((size_t)b * a.n_q + h) * a.head_dim;
+      out[i] = Elem<T>::from_f(acc * invL);
+    } else {   // un-normalised partial (M, L, O) for the cross-rank merge
+      float* out = reinterpret_cast<float*>(a.out) + (size_t)bh * (a.head_dim + 2);
+      out[2 + i] = acc;
+      if (i == 0) { out[0] = M; out[1] = L; }
+    }
+  }
+  pdl_launch_dependents();
+}
+template __global__ void merge_kernel<float>(MergeArgs);
+template __global__ void merge_kernel<__nv_bfloat16>(MergeArgs);
+
+// ---------------------------------------------------------------------------
+// Dense comparator cache write: k_cache[b, pos] = RoPE_pos(k_new[b]), v copy.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void dense_append_kernel(DenseAppendArgs a) {
+  const int b = blockIdx.x;
+  pdl_wait();
+  const int64_t pos = a.pos[b];
+  const T* k = reinterpret_cast<const T*>(a.k_new) + (size_t)b * a.D;
+  const T* v = reinterpret_cast<const T*>(a.v_new) + (size_t)b * a.D;
+  T* kc = reinterpret_cast<T*>(a.k_cache) + ((size_t)b * a.cap + pos) * a.D;
+  T* vc = reinterpret_cast<T*>(a.v_cache) + ((size_t)b * a.cap + pos) * a.D;
+  const int half = a.head_dim / 2;
+  for (int t = threadIdx.x; t < a.n_kv * half; t += blockDim.x) {
+    const int g = t / half, p = t % half;
+    int lo, hi; rope_pair(p, half, a.rope.style, lo, hi);
+    float c, s; rope_cs(a.rope.theta[p], pos, c, s);
+    const float xl = Elem<T>::to_f(k[g * a.head_dim + lo]), xh = Elem<T>::to_f(k[g * a.head_dim + hi]);
+    kc[g * a.head_dim + lo] = Elem<T>::from_f(xl * c - xh * s);
+    kc[g * a.head_dim + hi] = Elem<T>::from_f(xl * s + xh * c);
+  }
+  for (int i = threadIdx.x; i < a.D; i += blockDim.x) vc[i] = v[i];
+  pdl_launch_dependents();
+}
+template __global__ void dense_append_kernel<float>(DenseAppendArgs);
+template __global__ void dense_append_kernel<__nv_bfloat16>(DenseAppendArgs);
+
+// ---------------------------------------------------------------------------
+// Sharded: the rows this rank attends to = owned sinks, owned global picks,
+// owned recents (three ascending, disjoint, ordered ranges).  One CTA / request.
+// ---------------------------------------------------------------------------
+__global__ void owned_list_kernel(OwnedArgs a) {
+  const int b = blockIdx.x;
+  __shared__ int s_cnt[3], s_first;
+  pdl_wait();
+  const int s = a.seq_len[b];
+  const int64_t lo = a.shard_start, hi = a.shard_start + a.local_len[b];
+  const int gcnt = a.gcount[b];
+  const int* gs = a.gsel + (size_t)b * a.g_stride;
+  int* own = a.own_sel + (size_t)b * a.k;
+  // forced ranges (s > k only; when s <= k the global picks are every ranked token and
+  // the forced ranges are still [0,x) and [s-z,s) clipped to [0,s))
+  const int x = min(a.sink, s), z0 = max(x, s - a.recent);
+  const int64_t sk0 = max(lo, (int64_t)0), sk1 = min(hi, (int64_t)x);
+  const int64_t rc0 = max(lo, (int64_t)z0), rc1 = min(hi, (int64_t)s);
+  const int nsk = (int)max((int64_t)0, sk1 - sk0), nrc = (int)max((int64_t)0, rc1 - rc0);
+  if (threadIdx.x == 0) { s_cnt[0] = 0; s_first = gcnt; }
+  __syncthreads();
+  // global picks are ascending: owned ones form one contiguous run
+  for (int i = threadIdx.x; i < gcnt; i += blockDim.x) {
+    const int gi = gs[i];
+    if (gi >= lo && gi < hi) { atomicAdd(&s_cnt[0], 1); atomicMin(&s_first, i); }
+  }
+  __syncthreads();
+  const int ng = s_cnt[0], f = s_first;
+  for (int i = threadIdx.x; i < nsk; i += blockDim.x) own[i] = (int)(sk0 + i - lo);
+  for (int i = threadIdx.x; i < ng; i += blockDim.x) own[nsk + i] = (int)(gs[f + i] - lo);
+  for (int i = threadIdx.x; i < nrc; i += blockDim.x) own[nsk + ng + i] = (int)(rc0 + i - lo);
+  if (threadIdx.x == 0) a.own_count[b] = nsk + ng + nrc;
+  pdl_launch_dependents();
+}
+
+}  // namespace sals

@@ -1,0 +1,112 @@
+// Kernel argument structs and declarations shared by the kernels and the
+// host launcher (api.cu).  Internal to the library; the public boundary is
+// include/sals.h.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace sals {
+
+struct ProjectArgs {
+  const void* U;        // [D, r]
+  const void* x;        // append: k_new [B, D]; qproj: q [B, n_q*d]
+  int x_stride;
+  int D, r, ncols;      // ncols = r (append) or r* (qproj)
+  int B, head_dim, group, n_q;
+  int rows_per_cta;
+  // qproj outputs
+  float* out_f32;       // [B, r*]
+  float* qrope;         // [B, n_q, d]
+  const int* seq_len;   // [B]
+  RopeTable rope;
+  // append outputs
+  void* latent; int64_t cap; const int* pos;
+  const void* v_new; void* v_cache;
+};
+
+struct ScoreArgs {
+  const void* latent;   // [B, cap, r]
+  int64_t cap; int r, rstar;
+  const float* qtil;    // [B, r*]
+  const int* len;       // [B] tokens to score (s_b, or the shard's local length)
+  float* scores;        // [B, stride]
+  int64_t stride;
+  int tokens_per_cta;
+};
+
+struct TopkArgs {
+  const float* scores; int64_t score_stride;  // [B, stride]
+  const int* cand_idx;    // nullable: global index of each entry (-1 = empty)
+  const int* n_entries;   // nullable: entries of request b (else n_const)
+  int n_const;
+  const int* seq_len;     // [B] global s_b
+  int64_t idx_base;       // global index of entry 0 when cand_idx == nullptr
+  int k, sink, recent;
+  int mode;               // 0 = full Alg. 1 selection; 1 = ranked-range candidates only
+  int slice;              // entries per CTA
+  int* sel_out; int64_t sel_stride;
+  float* sel_score;       // nullable
+  int* sel_count;         // nullable [B]
+  int pad_to;             // -1 padding up to this many entries
+  int* sel_out2;          // nullable second copy of sel_out (user buffer), stride sel_stride
+  int seg_len;            // >0: entries are [world][B][seg_len] (all-gathered candidates)
+  int64_t seg_stride;     //     = B * seg_len
+};
+
+struct ReconArgs {        // SIMT reconstruct + RoPE (path S)
+  const void* latent; int64_t cap; int r;
+  const void* U;
+  const int* sel; const int* count; int k_stride;
+  int D, head_dim;
+  int64_t pos_base;       // global position of latent row 0 (shards)
+  RopeTable rope;
+  void* kr;               // [B*k_stride, D]
+};
+
+struct FlashArgs {        // split-K flash decode over a token list (sparse or dense)
+  const float* qrope;     // [B, n_q, d]
+  const void* kbase;      // dense: k_cache [B, cap, D]; sparse: K^R_C [B*k_stride, D]
+  const void* v_cache;    // [B, cap, D]
+  const int* sel;         // sparse: [B, k_stride] (local rows into v_cache)
+  const int* count;       // [B]
+  int64_t cap; int D, k_stride, n_q, n_kv, nsplit, chunk;
+  float scale_log2;
+  float* partials;        // [B, n_q, nsplit, d+2]
+  int64_t sel_row_base;   // subtract from sel entries to get the local v_cache row
+};
+
+struct MergeArgs {
+  const float* partials;
+  int64_t bh_stride, s_stride;
+  int nsplit, n_q, head_dim;
+  void* out;              // normalize: y [B, n_q*d] (T); else fp32 partial [B, n_q, d+2] (m, l, o)
+  int normalize;
+};
+
+struct DenseAppendArgs {
+  const void* k_new; const void* v_new; const int* pos;
+  void* k_cache; void* v_cache; int64_t cap;
+  int D, head_dim, n_kv;
+  RopeTable rope;
+};
+
+struct OwnedArgs {        // sharded: owned selection list = owned sinks | owned K9 picks | owned recents
+  const int* gsel; const int* gcount; int g_stride;
+  const int* seq_len; const int* local_len; int64_t shard_start;
+  int sink, recent, k;
+  int* own_sel; int* own_count;   // [B, k] local rows, [B]
+};
+
+template <typename T, bool POOL> __global__ void project_kernel(ProjectArgs a);
+template <typename T, int LG, int CPL> __global__ void latent_score_kernel(ScoreArgs a);
+__global__ void topk_cluster_kernel(TopkArgs a);
+template <typename T> __global__ void recon_rope_simt_kernel(ReconArgs a);
+template <typename T, int DH, int G, bool DENSE> __global__ void flash_decode_kernel(FlashArgs a);
+template <typename T> __global__ void merge_kernel(MergeArgs a);
+template <typename T> __global__ void dense_append_kernel(DenseAppendArgs a);
+__global__ void owned_list_kernel(OwnedArgs a);
+
+}  // namespace sals

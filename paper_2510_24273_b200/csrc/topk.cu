@@ -1,0 +1,210 @@
+// K4 / K9: TopK selection  C = TopK(p', k)   (Alg. 1 line 5)
+// with the sink / critical / recent policy and ties to the lower
+// index (reading R5).  One thread-block CLUSTER per request.
+//
+// Each CTA of the cluster loads a contiguous slice of the request's scores
+// into shared memory as order-preserving uint32 keys.  Four 8-bit radix
+// passes find the threshold key T (the need-th largest ranked key): per-warp
+// shared-memory histograms -> CTA histogram -> summed across the cluster
+// through DSMEM, and every CTA picks the same digit.  A final ordered
+// compaction writes, in ascending index order, every forced entry, every
+// ranked entry with key > T, and the first (need - #{key > T}) entries with
+// key == T (lowest indices first, counted across CTAs in rank order).
+//
+// mode 0 (sals_decode): entry e is token e; forced = [0,x) u [s-z,s); the
+//   k-x-z best of [x, s-z) are ranked; all s tokens when s <= k.
+// mode 1 (sharded): entries carry global indices (cand_idx, or idx_base + e);
+//   only the ranked range [x, s-z) takes part; up to k-x-z are selected.
+//   Used for a shard's local candidates and for the global select (K9) over
+//   the all-gathered candidates, which arrive in ascending index order.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sals {
+
+constexpr int kTopkThreads = 512;
+constexpr int kTopkWarps = kTopkThreads / 32;
+
+// Inclusive scan of one value per thread across the 512-thread block.
+__device__ __forceinline__ int block_incl_scan(int v, int* warp_tot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int n = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += n;
+  }
+  if (lane == 31) warp_tot[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    int t = (lane < kTopkWarps) ? warp_tot[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int n = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += n;
+    }
+    if (lane < kTopkWarps) warp_tot[lane] = t;   // inclusive warp prefix
+  }
+  __syncthreads();
+  const int add = (warp > 0) ? warp_tot[warp - 1] : 0;
+  const int r = v + add;
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kTopkThreads)
+topk_cluster_kernel(TopkArgs a) {
+  extern __shared__ __align__(16) uint8_t tk_smem[];
+  __shared__ uint32_t whist[kTopkWarps][256];
+  __shared__ uint32_t chist[2][256];
+  __shared__ int xch[4];           // cluster-visible: [0] ranked count, [1] definite count, [2] tie count
+  __shared__ int warp_tot[32];
+  __shared__ int s_digit, s_need;
+
+  const int CS = (int)cluster_nctarank();
+  const int rank = (int)cluster_ctarank();
+  const int b = blockIdx.x / CS;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int slice = a.slice;
+  uint32_t* keys = reinterpret_cast<uint32_t*>(tk_smem);
+  uint8_t* cls = tk_smem + (size_t)slice * 4;   // 0 none, 1 forced, 2 ranked
+  // global indices are only stored when they come from a candidate list
+  int* gidx = a.cand_idx ? reinterpret_cast<int*>(tk_smem + (size_t)slice * 5 + ((16 - (slice * 5) % 16) % 16))
+                         : nullptr;
+
+  pdl_wait();
+  const int s = a.seq_len[b];
+  const int n = a.n_entries ? a.n_entries[b] : (a.cand_idx ? a.n_const : s);
+  const int e0 = rank * slice;
+  const int nloc = max(0, min(slice, n - e0));
+  const int x = a.sink, z = a.recent;
+  const bool all_mode0 = (a.mode == 0) && (s <= a.k);
+
+  // ---- load slice -> keys / classes -------------------------------------
+  int my_ranked = 0;
+  for (int i = tid; i < nloc; i += kTopkThreads) {
+    const int e = e0 + i;
+    const size_t off = a.seg_len > 0 ? (size_t)(e / a.seg_len) * a.seg_stride + (size_t)b * a.seg_len + e % a.seg_len
+                                     : (size_t)b * a.score_stride + e;
+    const int idx = a.cand_idx ? a.cand_idx[off] : (int)(a.idx_base + e);
+    uint8_t c = 0;
+    if (idx >= 0 && idx < s) {
+      const bool in_rank = (idx >= x) && (idx < s - z);
+      if (a.mode == 0) c = (all_mode0 || !in_rank) ? 1 : 2;
+      else c = in_rank ? 2 : 0;
+    }
+    keys[i] = (c == 2) ? float_key(a.scores[off]) : 0u;
+    cls[i] = c;
+    if (gidx) gidx[i] = idx;
+    my_ranked += (c == 2);
+  }
+  {
+    int tot = block_incl_scan(my_ranked, warp_tot);
+    if (tid == kTopkThreads - 1) xch[0] = tot;
+  }
+  cluster_sync_all();
+  int n_ranked = 0;
+  for (int c = 0; c < CS; ++c) n_ranked += (int)ld_dsmem_u32(mapa_shared(smem_u32(&xch[0]), c));
+  int need = (a.mode == 0) ? (all_mode0 ? 0 : a.k - x - z) : (a.k - x - z);
+  need = max(0, min(need, n_ranked));
+
+  // ---- radix select of the threshold key T (4 x 8-bit passes) ------------
+  uint32_t T = 0xffffffffu;
+  int need_eq = 0;
+  if (need == n_ranked && need > 0) {
+    T = 0u; need_eq = n_ranked;          // every ranked entry is selected
+  } else if (need > 0) {
+    uint32_t prefix = 0;
+    int rem = need;
+    for (int pass = 0; pass < 4; ++pass) {
+      const int shift = 24 - 8 * pass;
+      for (int i = tid; i < kTopkWarps * 256; i += kTopkThreads) (&whist[0][0])[i] = 0;
+      __syncthreads();
+      for (int i = tid; i < nloc; i += kTopkThreads) {
+        if (cls[i] != 2) continue;
+        const uint32_t key = keys[i];
+        if (pass > 0 && ((key ^ prefix) >> (shift + 8)) != 0) continue;
+        atomicAdd(&whist[warp][(key >> shift) & 255u], 1u);
+      }
+      __syncthreads();
+      uint32_t* ch = chist[pass & 1];
+      if (tid < 256) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int w = 0; w < kTopkWarps; ++w) t += whist[w][tid];
+        ch[tid] = t;
+      }
+      cluster_sync_all();
+      // thread t (< 256) holds digit 255 - t; inclusive scan = count of digits >= it
+      int cnt = 0;
+      if (tid < 256) {
+        const uint32_t addr = smem_u32(&ch[255 - tid]);
+        for (int c = 0; c < CS; ++c) cnt += (int)ld_dsmem_u32(mapa_shared(addr, c));
+      }
+      const int incl = block_incl_scan(cnt, warp_tot);
+      const int excl = incl - cnt;
+      if (tid < 256 && excl < rem && rem <= incl) { s_digit = 255 - tid; s_need = rem - excl; }
+      __syncthreads();
+      prefix |= (uint32_t)s_digit << shift;
+      rem = s_need;
+      __syncthreads();
+    }
+    T = prefix;
+    need_eq = rem;
+  }
+
+  // ---- ordered compaction ------------------------------------------------
+  const int run = (nloc + kTopkThreads - 1) / kTopkThreads;
+  const int i0 = min(nloc, tid * run), i1 = min(nloc, i0 + run);
+  int n_def = 0, n_eq = 0;
+  for (int i = i0; i < i1; ++i) {
+    const uint8_t c = cls[i];
+    if (c == 1 || (c == 2 && keys[i] > T)) ++n_def;
+    else if (c == 2 && keys[i] == T) ++n_eq;
+  }
+  const int def_incl = block_incl_scan(n_def, warp_tot);
+  const int eq_incl = block_incl_scan(n_eq, warp_tot);
+  if (tid == kTopkThreads - 1) { xch[1] = def_incl; xch[2] = eq_incl; }
+  cluster_sync_all();
+  int def_before = 0, eq_before = 0, def_total = 0, eq_total = 0;
+  for (int c = 0; c < CS; ++c) {
+    const int dc = (int)ld_dsmem_u32(mapa_shared(smem_u32(&xch[1]), c));
+    const int ec = (int)ld_dsmem_u32(mapa_shared(smem_u32(&xch[2]), c));
+    if (c < rank) { def_before += dc; eq_before += ec; }
+    def_total += dc; eq_total += ec;
+  }
+  const int eq_local = xch[2];
+  const int take_local = max(0, min(need_eq - eq_before, eq_local));
+  const int out_base = def_before + min(need_eq, eq_before);
+  const int count = def_total + min(need_eq, eq_total);
+
+  int pos = out_base + (def_incl - n_def) + min(eq_incl - n_eq, take_local);
+  int eq_rank = eq_incl - n_eq;
+  int* out = a.sel_out + (size_t)b * a.sel_stride;
+  int* out2 = a.sel_out2 ? a.sel_out2 + (size_t)b * a.sel_stride : nullptr;
+  float* osc = a.sel_score ? a.sel_score + (size_t)b * a.sel_stride : nullptr;
+  for (int i = i0; i < i1; ++i) {
+    const uint8_t c = cls[i];
+    bool take = false;
+    if (c == 1 || (c == 2 && keys[i] > T)) take = true;
+    else if (c == 2 && keys[i] == T) { take = eq_rank < take_local; ++eq_rank; }
+    if (take) {
+      const int gi = gidx ? gidx[i] : (int)(a.idx_base + e0 + i);
+      out[pos] = gi;
+      if (out2) out2[pos] = gi;
+      if (osc) osc[pos] = key_float(keys[i]);
+      ++pos;
+    }
+  }
+  if (rank == CS - 1) {
+    for (int i = count + tid; i < a.pad_to; i += kTopkThreads) {
+      out[i] = -1;
+      if (out2) out2[i] = -1;
+      if (osc) osc[i] = -INFINITY;
+    }
+    if (tid == 0 && a.sel_count) a.sel_count[b] = count;
+  }
+  cluster_sync_all();   // keep shared memory alive until every peer finished its DSMEM reads
+  pdl_launch_dependents();
+}
+
+}  // namespace sals

@@ -1,0 +1,171 @@
+"""Thin ctypes binding of the C ABI in include/sals.h (argument marshalling only).
+
+Every function has the C name and forwards torch tensors as raw device
+pointers plus the current CUDA stream; all compute runs in libsals.so.  There
+is no fallback: importing this module without the in-tree library raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsals.so")
+
+SALS_F32, SALS_BF16 = 0, 1
+SALS_ROPE_HALF, SALS_ROPE_INTERLEAVED = 0, 1
+SALS_PATH_AUTO, SALS_PATH_SIMT, SALS_PATH_TCGEN05 = 0, 1, 2
+STATUS = {0: "SALS_OK", 1: "SALS_ERR_INVALID_ARGUMENT", 2: "SALS_ERR_UNSUPPORTED",
+          3: "SALS_ERR_WORKSPACE_TOO_SMALL", 4: "SALS_ERR_CUDA"}
+
+EXPORTED = ["sals_workspace_bytes", "sals_append_latent", "sals_decode", "sals_dense_append",
+            "sals_dense_workspace_bytes", "sals_dense_decode", "sals_shard_candidates", "sals_shard_attend",
+            "sals_merge_partials", "sals_shard_workspace_bytes", "sals_status_string", "sals_last_error",
+            "sals_launch_count"]
+
+
+class SalsError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class sals_config(ctypes.Structure):
+    _fields_ = [("num_q_heads", ctypes.c_int32), ("num_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+                ("rank", ctypes.c_int32), ("score_rank", ctypes.c_int32), ("top_k", ctypes.c_int32),
+                ("sink", ctypes.c_int32), ("recent", ctypes.c_int32), ("rope_base", ctypes.c_float),
+                ("rope_style", ctypes.c_int32), ("dtype", ctypes.c_int32), ("softmax_scale", ctypes.c_float),
+                ("path", ctypes.c_int32)]
+
+
+def make_config(*, num_q_heads, num_kv_heads, head_dim, rank, score_rank, top_k, sink=0, recent=0,
+                rope_base=10000.0, rope_style=SALS_ROPE_HALF, dtype="bf16", softmax_scale=0.0,
+                path=SALS_PATH_AUTO, **_unused) -> sals_config:
+    dt = {"bf16": SALS_BF16, "f32": SALS_F32, torch.bfloat16: SALS_BF16, torch.float32: SALS_F32}[dtype]
+    return sals_config(num_q_heads, num_kv_heads, head_dim, rank, score_rank, top_k, sink, recent,
+                       float(rope_base), rope_style, dt, float(softmax_scale), path)
+
+
+def torch_dtype(cfg: sals_config):
+    return torch.bfloat16 if cfg.dtype == SALS_BF16 else torch.float32
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2510_24273_b200.build` "
+                          "(or __graft_entry__.build()); there is no CPU fallback")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I32, I64, SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+    C = ctypes.POINTER(sals_config)
+    sig = {
+        "sals_workspace_bytes": (SZ, [C, I32, I32]),
+        "sals_append_latent": (I32, [C, P, P, P, I32, P, P, P, I64, P]),
+        "sals_decode": (I32, [C, P, P, P, P, I64, I32, P, I32, P, P, P, P, SZ, P]),
+        "sals_dense_append": (I32, [C, P, P, I32, P, P, P, I64, P]),
+        "sals_dense_workspace_bytes": (SZ, [C, I32, I32]),
+        "sals_dense_decode": (I32, [C, P, P, P, I64, I32, P, I32, P, P, SZ, P]),
+        "sals_shard_candidates": (I32, [C, P, P, P, I64, I32, I64, P, I32, P, P, P, P, SZ, P]),
+        "sals_shard_attend": (I32, [C, P, P, P, P, I64, I32, I64, P, I32, P, P, P, I32, P, P, SZ, P]),
+        "sals_merge_partials": (I32, [C, P, I32, I32, P, P]),
+        "sals_shard_workspace_bytes": (SZ, [C, I32, I32, I32]),
+        "sals_status_string": (ctypes.c_char_p, [I32]),
+        "sals_last_error": (ctypes.c_char_p, []),
+        "sals_launch_count": (ctypes.c_uint64, [I32]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype, f.argtypes = res, args
+    return lib
+
+
+_lib = _load()
+
+
+def _p(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _check(status: int):
+    if status != 0:
+        raise SalsError(status, _lib.sals_last_error().decode())
+
+
+def sals_workspace_bytes(cfg: sals_config, batch: int, max_seq_len: int) -> int:
+    return int(_lib.sals_workspace_bytes(ctypes.byref(cfg), batch, max_seq_len))
+
+
+def sals_dense_workspace_bytes(cfg: sals_config, batch: int, max_seq_len: int) -> int:
+    return int(_lib.sals_dense_workspace_bytes(ctypes.byref(cfg), batch, max_seq_len))
+
+
+def sals_shard_workspace_bytes(cfg: sals_config, batch: int, max_local_len: int, world: int) -> int:
+    return int(_lib.sals_shard_workspace_bytes(ctypes.byref(cfg), batch, max_local_len, world))
+
+
+def alloc_workspace(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+
+
+def sals_append_latent(cfg, U, k_new, v_new, pos, latent_cache, v_cache, stream=None):
+    B = k_new.shape[0]
+    _check(_lib.sals_append_latent(ctypes.byref(cfg), _p(U), _p(k_new), _p(v_new), B, _p(pos),
+                                   _p(latent_cache), _p(v_cache), latent_cache.shape[1], _stream(stream)))
+
+
+def sals_decode(cfg, U, q, latent_cache, v_cache, seq_len, max_seq_len, out, workspace,
+                sel_idx_out=None, scores_out=None, stream=None):
+    B = q.shape[0]
+    _check(_lib.sals_decode(ctypes.byref(cfg), _p(U), _p(q), _p(latent_cache), _p(v_cache), latent_cache.shape[1],
+                            B, _p(seq_len), int(max_seq_len), _p(out), _p(sel_idx_out), _p(scores_out),
+                            _p(workspace), workspace.numel(), _stream(stream)))
+
+
+def sals_dense_append(cfg, k_new, v_new, pos, k_cache, v_cache, stream=None):
+    _check(_lib.sals_dense_append(ctypes.byref(cfg), _p(k_new), _p(v_new), k_new.shape[0], _p(pos), _p(k_cache),
+                                  _p(v_cache), k_cache.shape[1], _stream(stream)))
+
+
+def sals_dense_decode(cfg, q, k_cache, v_cache, seq_len, max_seq_len, out, workspace, stream=None):
+    _check(_lib.sals_dense_decode(ctypes.byref(cfg), _p(q), _p(k_cache), _p(v_cache), k_cache.shape[1], q.shape[0],
+                                  _p(seq_len), int(max_seq_len), _p(out), _p(workspace), workspace.numel(),
+                                  _stream(stream)))
+
+
+def sals_shard_candidates(cfg, U, q, latent_shard, shard_start, local_len, max_local_len, seq_len,
+                          cand_score, cand_idx, workspace, stream=None):
+    _check(_lib.sals_shard_candidates(ctypes.byref(cfg), _p(U), _p(q), _p(latent_shard), latent_shard.shape[1],
+                                      q.shape[0], int(shard_start), _p(local_len), int(max_local_len), _p(seq_len),
+                                      _p(cand_score), _p(cand_idx), _p(workspace), workspace.numel(),
+                                      _stream(stream)))
+
+
+def sals_shard_attend(cfg, U, q, latent_shard, v_shard, shard_start, local_len, max_local_len, seq_len,
+                      cand_all_score, cand_all_idx, world, partial, workspace, stream=None):
+    _check(_lib.sals_shard_attend(ctypes.byref(cfg), _p(U), _p(q), _p(latent_shard), _p(v_shard),
+                                  latent_shard.shape[1], q.shape[0], int(shard_start), _p(local_len),
+                                  int(max_local_len), _p(seq_len), _p(cand_all_score), _p(cand_all_idx), int(world),
+                                  _p(partial), _p(workspace), workspace.numel(), _stream(stream)))
+
+
+def sals_merge_partials(cfg, partial_all, world, batch, out, stream=None):
+    _check(_lib.sals_merge_partials(ctypes.byref(cfg), _p(partial_all), int(world), int(batch), _p(out),
+                                    _stream(stream)))
+
+
+def sals_launch_count(reset: bool = False) -> int:
+    return int(_lib.sals_launch_count(1 if reset else 0))
+
+
+def sals_status_string(status: int) -> str:
+    return _lib.sals_status_string(status).decode()
+
+
+def sals_last_error() -> str:
+    return _lib.sals_last_error().decode()

@@ -1,0 +1,223 @@
+"""GPU parity of the CUDA path (through the C ABI) against the fp64 oracle.
+
+Small cases span several tiles / clusters and ragged tails; the paper-shaped
+configs c2-c4 run at BASELINE.json's full sizes with the launch configuration
+bench.py times (every output element is compared: the oracle is fast enough).
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import sals_oracle as O
+from tests import harness as H
+
+pytestmark = pytest.mark.gpu
+
+C = synth.CONFIGS
+
+
+def _shape(name, **over):
+    s = dict(C[name])
+    s.update(over)
+    return s
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    from paper_2510_24273_b200 import build
+    build.build()
+    assert torch.cuda.is_available()
+
+
+# ------------------------------------------------------------------ small / edge
+def test_c1_tiny_fp32():
+    r = H.full_check(_shape("c1"), 1, [256])
+    assert r["swaps"] == 0
+
+
+@pytest.mark.parametrize("path", [1, 0])
+def test_mha_ragged_batch(path):
+    sh = _shape("c2", num_q_heads=8, num_kv_heads=8, rank=256, score_rank=128, top_k=96)
+    H.full_check(sh, 5, [1, 37, 96, 97, 1500], path=path, seed=11)
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_gqa_groups(G):
+    sh = _shape("c3", num_q_heads=4 * G, num_kv_heads=4, rank=256, score_rank=128, top_k=200)
+    H.full_check(sh, 3, [700, 2049, 300], seed=12 + G)
+
+
+def test_sink_recent_policy():
+    sh = _shape("c2", num_q_heads=8, num_kv_heads=8, rank=128, score_rank=64, top_k=128)
+    H.full_check(sh, 2, [3000, 129], sink=16, recent=32, seed=13)
+
+
+def test_interleaved_rope_and_long_positions():
+    sh = _shape("c4", num_q_heads=8, num_kv_heads=2, rank=128, score_rank=64, top_k=256)
+    H.full_check(sh, 1, [70001], rope_style=1, seed=14)
+
+
+@pytest.mark.parametrize("hd", [64, 256])
+def test_head_dims(hd):
+    sh = _shape("c2", num_q_heads=4, num_kv_heads=4, head_dim=hd, rank=128, score_rank=64, top_k=64)
+    H.full_check(sh, 2, [500, 64], seed=15)
+
+
+def test_single_token_returns_value():
+    sh = _shape("c2", num_q_heads=4, num_kv_heads=4, rank=64, score_rank=32, top_k=16)
+    cfg, host, gpu = H.run_sals(sh, 1, [1], seed=16)
+    expect = host["v_new"][0]
+    assert np.max(np.abs(gpu["out"][0] - expect)) <= 2 ** -8 * np.abs(expect).max()
+    assert gpu["sel"][0][0] == 0 and np.all(gpu["sel"][0][1:] == -1)
+
+
+def test_topk_ties_lower_index():
+    """All-equal latent rows: every score ties, selection must be the first k tokens."""
+    from paper_2510_24273_b200 import sals
+    sh = _shape("c2", num_q_heads=4, num_kv_heads=4, rank=64, score_rank=32, top_k=40)
+    cfg = sals.make_config(**sh)
+    B, s = 2, 5000
+    U = torch.from_numpy(synth.orthonormal(np.random.default_rng(0), 512, 64).astype(np.float32)).cuda().bfloat16()
+    lat = torch.ones(B, s, 64, dtype=torch.bfloat16, device="cuda")
+    v = torch.randn(B, s, 512, device="cuda").bfloat16()
+    q = torch.randn(B, 512, device="cuda").bfloat16()
+    seq = torch.tensor([s, 3000], dtype=torch.int32, device="cuda")
+    ws = sals.alloc_workspace(sals.sals_workspace_bytes(cfg, B, s), "cuda")
+    out = torch.empty(B, 512, dtype=torch.bfloat16, device="cuda")
+    sel = torch.empty(B, 40, dtype=torch.int32, device="cuda")
+    sals.sals_decode(cfg, U, q, lat, v, seq, s, out, ws, sel_idx_out=sel)
+    assert sel.cpu().numpy().tolist() == [list(range(40))] * 2
+
+
+def test_graph_capture_replay_is_deterministic():
+    from paper_2510_24273_b200 import sals
+    sh = _shape("c3", rank=256, score_rank=128, top_k=512)
+    cfg = sals.make_config(**sh)
+    B, s = 2, 4000
+    p = synth.gen_problem(num_q_heads=32, num_kv_heads=8, head_dim=128, rank=256, batch=B, seq_lens=[s, s], seed=3)
+    dev = lambda a: torch.from_numpy(a).cuda().bfloat16()
+    U, lat, v, q = dev(p["U"]), dev(p["latent"]), dev(p["v"]), dev(p["q"])
+    seq = torch.tensor([s, s], dtype=torch.int32, device="cuda")
+    ws = sals.alloc_workspace(sals.sals_workspace_bytes(cfg, B, s), "cuda")
+    out = torch.empty(B, 32 * 128, dtype=torch.bfloat16, device="cuda")
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        sals.sals_decode(cfg, U, q, lat, v, seq, s, out, ws)
+        st.synchronize()
+        ref = out.clone()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            sals.sals_decode(cfg, U, q, lat, v, seq, s, out, ws)
+        for _ in range(3):
+            out.zero_()
+            g.replay()
+        st.synchronize()
+    assert torch.equal(out, ref)
+
+
+# ------------------------------------------------------------------ full sizes
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_full_size_configs(name):
+    sh = _shape(name)
+    s = sh["seq"]
+    B = sh["batch"]
+    r = H.full_check(sh, B, [s] * B, seed=synth.SEED_BASE + int(name[1]))
+    print(name, r)
+
+
+def test_full_size_ragged_c3():
+    sh = _shape("c3")
+    H.full_check(sh, 4, [32768, 17, 4096, 30001], seed=21)
+
+
+# ------------------------------------------------------------------ dense comparator
+@pytest.mark.parametrize("dtype,G", [("bf16", 1), ("bf16", 4), ("f32", 2)])
+def test_dense_decode(dtype, G):
+    """Dense flash decode over a post-RoPE cache (cache rows written by the oracle's
+    dense append and rounded to the storage dtype) vs the oracle's dense decode."""
+    from paper_2510_24273_b200 import sals
+    nkv, d = 4, (128 if dtype == "bf16" else 64)
+    sh = dict(num_q_heads=nkv * G, num_kv_heads=nkv, head_dim=d, rank=64, score_rank=32, top_k=64,
+              rope_base=5e5, dtype=dtype)
+    cfg = sals.make_config(**sh)
+    oc = O.Config(num_q_heads=nkv * G, num_kv_heads=nkv, head_dim=d, rank=64, score_rank=32, top_k=64, rope_base=5e5)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    rng = np.random.default_rng(5)
+    B, cap = 3, 3000
+    seq_lens = np.array([3000, 1, 1777], dtype=np.int32)
+    D = nkv * d
+    K = rng.standard_normal((B, cap, D))
+    kc_ref = np.stack([O.dense_append_key(oc, K[b], np.arange(cap)) for b in range(B)])
+    kc = torch.from_numpy(kc_ref.astype(np.float32)).cuda().to(tdt)
+    vc = torch.from_numpy(rng.standard_normal((B, cap, D)).astype(np.float32)).cuda().to(tdt)
+    qt = torch.from_numpy(rng.standard_normal((B, nkv * G * d)).astype(np.float32)).cuda().to(tdt)
+    seq = torch.from_numpy(seq_lens).cuda()
+    ws = sals.alloc_workspace(sals.sals_dense_workspace_bytes(cfg, B, cap), "cuda")
+    out = torch.empty(B, nkv * G * d, dtype=tdt, device="cuda")
+    sals.sals_dense_decode(cfg, qt, kc, vc, seq, cap, out, ws)
+    torch.cuda.synchronize()
+    y = O.dense_decode(oc, H.widen(qt), H.widen(kc), H.widen(vc), seq_lens)
+    H.check_output(H.widen(out), y, dtype)
+
+
+def test_dense_append_positions():
+    from paper_2510_24273_b200 import sals
+    sh = dict(num_q_heads=8, num_kv_heads=2, head_dim=128, rank=64, score_rank=32, top_k=64, rope_base=5e5)
+    cfg = sals.make_config(**sh)
+    rng = np.random.default_rng(6)
+    B, cap = 4, 140000
+    pos = np.array([0, 1, 70000, 131071], dtype=np.int32)
+    k = torch.from_numpy(rng.standard_normal((B, 256)).astype(np.float32)).cuda().bfloat16()
+    v = torch.from_numpy(rng.standard_normal((B, 256)).astype(np.float32)).cuda().bfloat16()
+    kc = torch.zeros(B, cap, 256, dtype=torch.bfloat16, device="cuda")
+    vc = torch.zeros_like(kc)
+    sals.sals_dense_append(cfg, k, v, torch.from_numpy(pos).cuda(), kc, vc)
+    oc = O.Config(num_q_heads=8, num_kv_heads=2, head_dim=128, rank=64, score_rank=32, top_k=64, rope_base=5e5)
+    ref = O.dense_append_key(oc, H.widen(k), pos)
+    got = np.stack([H.widen(kc[b, pos[b]]) for b in range(B)])
+    ulp = 2.0 ** (np.floor(np.log2(np.maximum(np.abs(ref), 1e-30))) - 7)
+    assert np.all(np.abs(got - ref) <= ulp + 1e-5)
+
+
+# ------------------------------------------------------------------ sharded (virtual ranks)
+@pytest.mark.parametrize("P,sink,recent", [(2, 0, 0), (4, 16, 64), (3, 0, 8)])
+def test_sharded_virtual_ranks_equal_unsharded(P, sink, recent):
+    from paper_2510_24273_b200 import sals
+    sh = _shape("c4", rank=256, score_rank=128, top_k=1024)
+    B, s = 2, 20000
+    cfg, host, gpu = H.run_sals(sh, B, [s, s - 3333], sink=sink, recent=recent, seed=31)
+    oc = H.oracle_cfg(sh, sink, recent)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda().bfloat16()
+    U, q = dev(host["U"]), dev(host["q"])
+    seq = torch.from_numpy(host["seq_len"]).cuda()
+    k = sh["top_k"]
+    bounds = np.linspace(0, s, P + 1).astype(int)
+    cands_s, cands_i, wss, shards = [], [], [], []
+    for p in range(P):
+        a, b_ = bounds[p], bounds[p + 1]
+        lat = dev(host["latent"][:, a:b_])
+        vv = dev(host["v"][:, a:b_])
+        loc = np.clip(host["seq_len"] - a, 0, b_ - a).astype(np.int32)
+        locd = torch.from_numpy(loc).cuda()
+        ws = sals.alloc_workspace(sals.sals_shard_workspace_bytes(cfg, B, b_ - a, P), "cuda")
+        cs = torch.empty(B, k, dtype=torch.float32, device="cuda")
+        ci = torch.empty(B, k, dtype=torch.int32, device="cuda")
+        sals.sals_shard_candidates(cfg, U, q, lat, int(a), locd, b_ - a, seq, cs, ci, ws)
+        cands_s.append(cs); cands_i.append(ci); wss.append(ws); shards.append((a, b_, lat, vv, locd))
+    all_s = torch.stack(cands_s).contiguous()
+    all_i = torch.stack(cands_i).contiguous()
+    parts = []
+    for p in range(P):
+        a, b_, lat, vv, locd = shards[p]
+        part = torch.empty(B, sh["num_q_heads"], sh["head_dim"] + 2, dtype=torch.float32, device="cuda")
+        sals.sals_shard_attend(cfg, U, q, lat, vv, int(a), locd, b_ - a, seq, all_s, all_i, P, part, wss[p])
+        parts.append(part)
+    out = torch.empty(B, sh["num_q_heads"] * sh["head_dim"], dtype=torch.bfloat16, device="cuda")
+    sals.sals_merge_partials(cfg, torch.stack(parts).contiguous(), P, B, out)
+    torch.cuda.synchronize()
+    # same selection as the unsharded GPU decode => output equal up to fp32 merge order
+    forced = [gpu["sel"][b][gpu["sel"][b] >= 0].astype(np.int64) for b in range(B)]
+    orc = O.decode(oc, host["U"], host["q"], host["latent"], host["v"], host["seq_len"], forced_selection=forced)
+    H.check_output(H.widen(out), orc["y"], "bf16")
+    assert np.max(np.abs(H.widen(out) - gpu["out"])) <= 2 ** -6
