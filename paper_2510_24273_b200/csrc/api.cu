@@ -41,7 +41,7 @@ cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
   attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attrs[na].val.programmaticStreamSerializationAllowed = 1;
   ++na;
-  if (cluster > 1) {
+  if (cluster >= 1) {
     attrs[na].id = cudaLaunchAttributeClusterDimension;
     attrs[na].val.clusterDim.x = cluster;
     attrs[na].val.clusterDim.y = 1;
@@ -197,6 +197,12 @@ sals_status launch_project(const sals_config* c, const Plan& p, bool pool, Proje
   a.rows_per_cta = p.proj_rows;
   const int ncolblk = ceil_div(ncols, 64);
   dim3 grid(p.proj_cs, ncolblk + (pool ? 1 : 0));
+  static bool attr_done = false;
+  if (!attr_done) {
+    SALS_CUDA_TRY(cudaFuncSetAttribute(project_kernel<T, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    SALS_CUDA_TRY(cudaFuncSetAttribute(project_kernel<T, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr_done = true;
+  }
   if (pool) SALS_CUDA_TRY(launch(project_kernel<T, true>, grid, dim3(128), 0, st, p.proj_cs, a));
   else SALS_CUDA_TRY(launch(project_kernel<T, false>, grid, dim3(128), 0, st, p.proj_cs, a));
   return SALS_OK;
@@ -229,7 +235,7 @@ sals_status launch_score(const sals_config* c, ScoreArgs a, int batch, int max_l
     case 324: k = latent_score_kernel<T, 32, 4>; break;
     default: return fail(SALS_ERR_UNSUPPORTED, "score rank layout");
   }
-  SALS_CUDA_TRY(launch(k, grid, dim3(256), 0, st, 1, a));
+  SALS_CUDA_TRY(launch(k, grid, dim3(256), 0, st, 0, a));
   return SALS_OK;
 }
 
@@ -240,7 +246,7 @@ sals_status launch_topk(const TopkArgs& a, int batch, int cs, size_t smem, cudaS
     SALS_CUDA_TRY(cudaFuncSetAttribute(topk_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr_done = true;
   }
-  SALS_CUDA_TRY(launch(topk_cluster_kernel, dim3(batch * cs), dim3(512), smem, st, cs, a));
+  SALS_CUDA_TRY(launch(topk_cluster_kernel, dim3(batch * cs), dim3(512), smem, st, cs, a));  // cluster attr even for cs == 1
   return SALS_OK;
 }
 
@@ -254,7 +260,7 @@ sals_status launch_recon_simt(const sals_config* c, ReconArgs a, int batch, int 
     attr_done = true;
   }
   dim3 grid(ceil_div(kmax, 32), c->num_kv_heads, batch);
-  SALS_CUDA_TRY(launch(recon_rope_simt_kernel<T>, grid, dim3(256), smem, st, 1, a));
+  SALS_CUDA_TRY(launch(recon_rope_simt_kernel<T>, grid, dim3(256), smem, st, 0, a));
   return SALS_OK;
 }
 
@@ -279,13 +285,13 @@ sals_status launch_flash(const sals_config* c, FlashArgs a, int batch, cudaStrea
 #undef SALS_FD_CASE
   if (!k) return fail(SALS_ERR_UNSUPPORTED, "flash decode shape");
   dim3 grid(ceil_div(a.nsplit, 4), c->num_kv_heads, batch);
-  SALS_CUDA_TRY(launch(k, grid, dim3(128), 0, st, 1, a));
+  SALS_CUDA_TRY(launch(k, grid, dim3(128), 0, st, 0, a));
   return SALS_OK;
 }
 
 template <typename T>
 sals_status launch_merge(const sals_config* c, MergeArgs a, int batch, cudaStream_t st) {
-  SALS_CUDA_TRY(launch(merge_kernel<T>, dim3(batch * c->num_q_heads), dim3(std::max(32, c->head_dim)), 0, st, 1, a));
+  SALS_CUDA_TRY(launch(merge_kernel<T>, dim3(batch * c->num_q_heads), dim3(std::max(32, c->head_dim)), 0, st, 0, a));
   return SALS_OK;
 }
 
@@ -463,8 +469,8 @@ sals_status sals_dense_append(const sals_config* cfg, const void* k_new, const v
   a.D = cfg->num_kv_heads * cfg->head_dim; a.head_dim = cfg->head_dim; a.n_kv = cfg->num_kv_heads;
   a.rope = make_rope(cfg);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (cfg->dtype == SALS_BF16) SALS_CUDA_TRY(launch(dense_append_kernel<__nv_bfloat16>, dim3(batch), dim3(256), 0, st, 1, a));
-  else SALS_CUDA_TRY(launch(dense_append_kernel<float>, dim3(batch), dim3(256), 0, st, 1, a));
+  if (cfg->dtype == SALS_BF16) SALS_CUDA_TRY(launch(dense_append_kernel<__nv_bfloat16>, dim3(batch), dim3(256), 0, st, 0, a));
+  else SALS_CUDA_TRY(launch(dense_append_kernel<float>, dim3(batch), dim3(256), 0, st, 0, a));
   return SALS_OK;
 }
 
@@ -604,7 +610,7 @@ sals_status sals_shard_attend(const sals_config* cfg, const void* U, const void*
   oa.gsel = gsel; oa.gcount = gcount; oa.g_stride = cfg->top_k; oa.seq_len = d_seq_len; oa.local_len = d_local_len;
   oa.shard_start = shard_start; oa.sink = cfg->sink; oa.recent = cfg->recent; oa.k = cfg->top_k;
   oa.own_sel = own; oa.own_count = own_count;
-  SALS_CUDA_TRY(launch(owned_list_kernel, dim3(batch), dim3(256), 0, st, 1, oa));
+  SALS_CUDA_TRY(launch(owned_list_kernel, dim3(batch), dim3(256), 0, st, 0, oa));
   if (cfg->dtype == SALS_BF16)
     return attend_list<__nv_bfloat16>(cfg, p, U, latent_shard, v_shard, cap_local, batch, shard_start, own,
                                       own_count, ws, nullptr, partial, st);

@@ -4,6 +4,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 namespace sals {
 
@@ -82,7 +83,12 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
 __device__ __forceinline__ uint32_t cluster_nctarank() {
   uint32_t r; asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r)); return r;
 }
+// Full barrier of every thread of every CTA of the cluster, with release /
+// acquire ordering of shared (and DSMEM) accesses.  The leading __syncthreads
+// keeps the CTA-local ordering explicit also for kernels launched without a
+// cluster attribute (an implicit 1-CTA cluster).
 __device__ __forceinline__ void cluster_sync_all() {
+  __syncthreads();
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 // Map a local shared-memory address to the same offset in CTA `rank` of the cluster.

@@ -58,7 +58,7 @@ topk_cluster_kernel(TopkArgs a) {
   __shared__ uint32_t chist[2][256];
   __shared__ int xch[4];           // cluster-visible: [0] ranked count, [1] definite count, [2] tie count
   __shared__ int warp_tot[32];
-  __shared__ int s_digit, s_need;
+  __shared__ int s_digit, s_need, s_nranked;
 
   const int CS = (int)cluster_nctarank();
   const int rank = (int)cluster_ctarank();
@@ -102,10 +102,17 @@ topk_cluster_kernel(TopkArgs a) {
     if (tid == kTopkThreads - 1) xch[0] = tot;
   }
   cluster_sync_all();
-  int n_ranked = 0;
-  for (int c = 0; c < CS; ++c) n_ranked += (int)ld_dsmem_u32(mapa_shared(smem_u32(&xch[0]), c));
-  int need = (a.mode == 0) ? (all_mode0 ? 0 : a.k - x - z) : (a.k - x - z);
-  need = max(0, min(need, n_ranked));
+  if (tid == 0) {
+    int nr = 0;
+    for (int c = 0; c < CS; ++c) nr += (int)ld_dsmem_u32(mapa_shared(smem_u32(&xch[0]), c));
+    int nd = (a.mode == 0) ? (all_mode0 ? 0 : a.k - x - z) : (a.k - x - z);
+    s_nranked = nr;
+    s_need = max(0, min(nd, nr));
+  }
+  __syncthreads();
+  const int n_ranked = s_nranked;
+  const int need = s_need;
+  __syncthreads();
 
   // ---- radix select of the threshold key T (4 x 8-bit passes) ------------
   uint32_t T = 0xffffffffu;
@@ -140,6 +147,7 @@ topk_cluster_kernel(TopkArgs a) {
         const uint32_t addr = smem_u32(&ch[255 - tid]);
         for (int c = 0; c < CS; ++c) cnt += (int)ld_dsmem_u32(mapa_shared(addr, c));
       }
+      if (tid == 0) { s_digit = 0; s_need = 0; }
       const int incl = block_incl_scan(cnt, warp_tot);
       const int excl = incl - cnt;
       if (tid < 256 && excl < rem && rem <= incl) { s_digit = 255 - tid; s_need = rem - excl; }
