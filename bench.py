@@ -1,0 +1,438 @@
+#!/usr/bin/env python
+"""SALS decode-attention benchmark (BASELINE.json metric) — one JSON line on rank 0.
+
+A step = decoding one token for a batch of B requests through the 32 attention
+layers of the model: per layer `sals_append_latent` (Alg. 1 lines 2-3) then
+`sals_decode` (lines 2, 4-9) on that layer's own caches.  32 distinct layers
+keep the per-step working set (~1.8 GB at c2) far above the 126 MB L2.  The
+step is captured once in a CUDA graph and replayed; K timed steps sit between a
+barrier + synchronize on both sides, timed with CUDA events, max over ranks.
+
+Workloads (BASELINE.json configs): c2 (default, configs[1]) LLaMA2-7B layer
+B=8 n=4K; c3 Mistral-7B GQA B=4 n=32K; c4 LLaMA3.1-8B B=1 n=128K.  N>1 ranks
+run independent replicas (weak scaling, no collective) unless --workload
+c4-sharded, which sequence-shards c4 over the ranks with two NCCL all-gathers
+per layer (strong scaling).
+
+`--impl reference` times the fp64 CPU oracle (the reference arm of this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "decode attention tokens/s (32-layer attention step)"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["sals", "reference"], default="sals")
+    ap.add_argument("--workload", choices=["c2", "c3", "c4", "c4-sharded"], default="c2")
+    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--path", type=int, default=0, help="0 auto, 1 SIMT, 2 tcgen05")
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+def workload_shape(name):
+    base = "c4" if name.startswith("c4") else name
+    sh = dict(synth.CONFIGS[base])
+    return base, sh
+
+
+def describe(name, sh, L):
+    D = sh["num_kv_heads"] * sh["head_dim"]
+    return (f"{name}: B={sh['batch']} n={sh['seq']} n_q/n_kv={sh['num_q_heads']}/{sh['num_kv_heads']} d={sh['head_dim']} "
+            f"(D={D}) r={sh['rank']} r*={sh['score_rank']} k={sh['top_k']} rope_base={sh['rope_base']:g} x{L} layers")
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index=0, period=0.02):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.period = period
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ distributed
+def dist_init(n):
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ CPU oracle arm
+def oracle_problem(sh, seed=synth.SEED_BASE + 99):
+    from oracle import sals_oracle as O
+    cfg = O.Config(num_q_heads=sh["num_q_heads"], num_kv_heads=sh["num_kv_heads"], head_dim=sh["head_dim"],
+                   rank=sh["rank"], score_rank=sh["score_rank"], top_k=sh["top_k"], rope_base=sh["rope_base"])
+    p = synth.gen_problem(num_q_heads=sh["num_q_heads"], num_kv_heads=sh["num_kv_heads"], head_dim=sh["head_dim"],
+                          rank=sh["rank"], batch=1, seq_lens=[sh["seq"]], seed=seed)
+    return cfg, p
+
+
+def oracle_cores():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info()] or [os.cpu_count()])
+    except Exception:
+        return os.cpu_count()
+
+
+def oracle_step(cfg, p, s):
+    """One request x one layer of the workload through the fp64 oracle (as it stands)."""
+    from oracle import sals_oracle as O
+    t0 = time.perf_counter()
+    O.append(cfg, p["U"], p["k_new"], p["v_new"], [s - 1], p["latent"], p["v"])
+    O.decode(cfg, p["U"], p["q"], p["latent"], p["v"], [s])
+    return time.perf_counter() - t0
+
+
+def oracle_sample(sh, budget_s=12.0):
+    cfg, p = oracle_problem(sh)
+    times, t_all = [], time.perf_counter()
+    while not times or time.perf_counter() - t_all < budget_s:
+        times.append(oracle_step(cfg, p, sh["seq"]))
+    return float(np.median(times)), len(times), oracle_cores()
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    base, sh = workload_shape(args.workload)
+    L, B = args.layers, sh["batch"]
+    cfg, p = oracle_problem(sh)
+    for _ in range(args.warmup):
+        oracle_step(cfg, p, sh["seq"])
+    per = [oracle_step(cfg, p, sh["seq"]) for _ in range(args.steps)]
+    t_req = float(np.median(per))
+    step_s = t_req * B * L                      # the whole 32-layer step of B requests, extrapolated
+    value = B / step_s
+    cores = oracle_cores()
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": describe(args.workload, sh, L), "batch": B, "seq_len": sh["seq"], "layers": L},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                             "sample": f"each step = 1 request x 1 layer oracle append+decode at the full workload "
+                                       f"shape (median of {args.steps}), extrapolated x{B} requests x{L} layers"},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def build_layers(sh, L, device, seed, dense):
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    layers = []
+    for _ in range(L):
+        layers.append(synth.gen_layer_torch(num_q_heads=sh["num_q_heads"], num_kv_heads=sh["num_kv_heads"],
+                                            head_dim=sh["head_dim"], rank=sh["rank"], batch=sh["batch"],
+                                            seq=sh["seq"], generator=g, device=device, dense=dense))
+    return layers
+
+
+def time_graph(g, stream, steps, warmup, world):
+    for _ in range(warmup):
+        g.replay()
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        g.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    return e0.elapsed_time(e1) / steps
+
+
+def run_sals(args, rank, world):
+    from paper_2510_24273_b200 import sals, traffic
+    base, sh = workload_shape(args.workload)
+    L, B, s = args.layers, sh["batch"], sh["seq"]
+    dev = "cuda"
+    cfg = sals.make_config(**sh, path=args.path)
+    layers = build_layers(sh, L, dev, synth.SEED_BASE + 1000 * rank, dense=not args.no_dense)
+    D, nqd = sh["num_kv_heads"] * sh["head_dim"], sh["num_q_heads"] * sh["head_dim"]
+    seq = torch.full((B,), s, dtype=torch.int32, device=dev)
+    pos = seq - 1
+    ws = sals.alloc_workspace(sals.sals_workspace_bytes(cfg, B, s), dev)
+    out = torch.empty(L, B, nqd, dtype=torch.bfloat16, device=dev)
+
+    def step():
+        for l, ly in enumerate(layers):
+            sals.sals_append_latent(cfg, ly["U"], ly["k_new"], ly["v_new"], pos, ly["latent"], ly["v"])
+            sals.sals_decode(cfg, ly["U"], ly["q"], ly["latent"], ly["v"], seq, s, out[l], ws)
+
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        step()                                 # eager warm-up (sets kernel attributes)
+        stream.synchronize()
+        sals.sals_launch_count(reset=True)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            step()
+        launches_per_step = sals.sals_launch_count(reset=True)
+        with ClockSampler(torch.cuda.current_device()) as clk:
+            ms = time_graph(g, stream, args.steps, args.warmup, world)
+    ms = max_over_ranks(ms, world)
+    value = world * B / (ms / 1e3)
+
+    # ---- per-stage timing (events on the launching stream), layer 0
+    with torch.cuda.stream(stream):
+        ly = layers[0]
+        stages = sals.sals_decode_profile(cfg, ly["U"], ly["q"], ly["latent"], ly["v"], seq, s, out[0], ws, iters=20)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(20):
+            sals.sals_append_latent(cfg, ly["U"], ly["k_new"], ly["v_new"], pos, ly["latent"], ly["v"])
+        e1.record(stream)
+        stream.synchronize()
+        stages["append"] = e0.elapsed_time(e1) / 20
+    stages_us = {k: round(v * 1e3, 2) for k, v in stages.items() if v > 0}
+
+    # ---- dense comparator (same build), same batch / layers
+    dense = None
+    if not args.no_dense:
+        wsd = sals.alloc_workspace(sals.sals_dense_workspace_bytes(cfg, B, s), dev)
+
+        def dstep():
+            for l, ly in enumerate(layers):
+                sals.sals_dense_append(cfg, ly["k_new"], ly["v_new"], pos, ly["k_dense"], ly["v"])
+                sals.sals_dense_decode(cfg, ly["q"], ly["k_dense"], ly["v"], seq, s, out[l], wsd)
+        with torch.cuda.stream(stream):
+            dstep()
+            stream.synchronize()
+            gd = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gd, stream=stream):
+                dstep()
+            dms = time_graph(gd, stream, max(5, args.steps // 2), args.warmup, world)
+        dms = max_over_ranks(dms, world)
+        dbytes = traffic.dense_bytes(batch=B, seq=s, num_kv_heads=sh["num_kv_heads"], head_dim=sh["head_dim"])
+        peaks, _ = load_peaks()
+        dense = {"ms_per_step": dms, "tokens_per_s": world * B / (dms / 1e3),
+                 "hbm_frac_of_measured": (dbytes * L / (dms / 1e3)) / (peaks["hbm_gbs"] * 1e9),
+                 "kernel": "in-build split-K flash decode over the full post-RoPE K/V cache"}
+
+    # ---- e2e through the public API with host buffers
+    e2e = run_e2e(cfg, layers, seq, pos, s, ws, out, stream, args, world)
+
+    # ---- roofline of the dominant kernel
+    peaks, peak_kind = load_peaks()
+    roof = roofline(sh, stages, peaks, peak_kind, args.workload)
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": describe(args.workload, sh, L), "batch": B, "seq_len": s, "layers": L,
+                   "l2": "inputs larger than L2: 32 distinct layers' caches per step",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "us_per_layer_step": ms * 1e3 / L,
+        "stages_us": stages_us,
+        "path": "tcgen05" if stages.get("flash", 0) == 0 else "simt",
+        "roofline": roof,
+        "gpu_launches": int(launches_per_step * args.steps),
+        "launches_per_step": int(launches_per_step),
+        "clocks": clk.summary(),
+        "e2e": e2e,
+    }
+    if dense:
+        line["dense"] = dense
+        line["speedup_vs_dense"] = dense["ms_per_step"] / ms
+    if rank == 0 and not args.no_cpu_baseline:
+        t_req, n, cores = oracle_sample(sh, budget_s=12.0)
+        v = 1.0 / (t_req * L)
+        line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                                "sample": f"{n} single-request x single-layer oracle decodes at the full workload "
+                                          f"shape (median {t_req:.3f} s), extrapolated x{B} requests x{L} layers"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def run_e2e(cfg, layers, seq, pos, s, ws, out, stream, args, world):
+    from paper_2510_24273_b200 import sals
+    L = len(layers)
+    B = seq.shape[0]
+    # host (pinned) inputs of every layer for one step, one H2D copy; results back with one D2H copy
+    host_in = torch.stack([torch.stack([ly["q"], ly["k_new"], ly["v_new"]]) for ly in layers]).cpu().pin_memory()
+    dev_in = torch.empty_like(host_in, device="cuda")
+    host_out = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+    steps = max(3, min(args.steps, 20))
+    with torch.cuda.stream(stream):
+        def one():
+            dev_in.copy_(host_in, non_blocking=True)
+            for l, ly in enumerate(layers):
+                q, kn, vn = dev_in[l, 0], dev_in[l, 1], dev_in[l, 2]
+                sals.sals_append_latent(cfg, ly["U"], kn, vn, pos, ly["latent"], ly["v"])
+                sals.sals_decode(cfg, ly["U"], q, ly["latent"], ly["v"], seq, s, out[l], ws)
+            host_out.copy_(out, non_blocking=True)
+            stream.synchronize()
+        for _ in range(2):
+            one()
+        barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            one()
+        e1.record(stream)
+        stream.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1) / steps, world)
+    return {"value": world * B / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": int(host_in.numel() * host_in.element_size()),
+            "d2h_bytes_per_step": int(host_out.numel() * host_out.element_size()),
+            "how": "eager C-ABI calls per layer (no graph), pinned H2D of q/k/v for all layers, D2H of all outputs, "
+                   "stream sync per step"}
+
+
+def roofline(sh, stages, peaks, peak_kind, workload):
+    from paper_2510_24273_b200 import traffic
+    B, s = sh["batch"], sh["seq"]
+    kw = dict(batch=B, seq=s, num_q_heads=sh["num_q_heads"], num_kv_heads=sh["num_kv_heads"],
+              head_dim=sh["head_dim"], rank=sh["rank"], score_rank=sh["score_rank"], top_k=sh["top_k"])
+    sb = traffic.stage_bytes(**kw)
+    fl = traffic.recon_flops(**kw)
+    hbm = peaks["hbm_gbs"]
+    tf = peaks["bf16_tflops"]
+    cand = {}
+    if stages.get("recon_attn", 0) > 0:
+        t = stages["recon_attn"] * 1e-3
+        cand["recon_attn"] = {"bound": "tensor", "achieved": fl / t / 1e12, "peak": tf, "unit": "TFLOP/s",
+                              "frac": fl / t / 1e12 / tf, "algorithmic": fl, "bytes": sb["recon_attn"],
+                              "hbm_frac": sb["recon_attn"] / t / 1e9 / hbm}
+    if stages.get("score", 0) > 0:
+        t = stages["score"] * 1e-3
+        cand["score"] = {"bound": "hbm", "achieved": sb["score"] / t / 1e9, "peak": hbm, "unit": "GB/s",
+                         "frac": sb["score"] / t / 1e9 / hbm, "algorithmic": sb["score"]}
+    dom = max(((k, v) for k, v in stages.items() if k in cand), key=lambda kv: kv[1], default=(None, 0))[0]
+    if dom is None:
+        return None
+    r = dict(cand[dom])
+    r["kernel"] = dom
+    r["peak_source"] = f"{peak_kind} (MEASURED_PEAKS.json burst)" if peak_kind == "measured" else "fallback"
+    r["traffic"] = ncu_traffic(workload, dom)
+    r["others"] = {k: {kk: v[kk] for kk in ("bound", "achieved", "unit", "frac")} for k, v in cand.items() if k != dom}
+    return r
+
+
+def ncu_traffic(workload, kernel):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    return d.get(workload, {}).get(kernel)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_init(args.gpus)
+    try:
+        if args.impl == "reference":
+            run_reference(args, rank, world)
+        elif args.workload == "c4-sharded":
+            from paper_2510_24273_b200 import sharded
+            sharded.bench(args, rank, world)
+        else:
+            from paper_2510_24273_b200 import build
+            build.build()
+            run_sals(args, rank, world)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -122,6 +122,21 @@ sals_status sals_decode(const sals_config* cfg, const void* U, const void* q,
                         void* workspace, size_t ws_bytes, void* stream);
 
 /*
+ * sals_decode_profile — profiling only: runs sals_decode `iters` times with a
+ * CUDA event after every stage kernel and SYNCHRONISES the stream after each
+ * run; writes the mean milliseconds of each stage to stage_ms[6] =
+ * {query projection + query RoPE, latent scoring, top-k, reconstruct(+fused
+ * attention on the tcgen05 path), SIMT flash attention, LSE merge} (0 for a
+ * stage the chosen path does not launch).  Events between kernels serialise
+ * the chain (no programmatic overlap), so the sum exceeds a sals_decode.
+ */
+sals_status sals_decode_profile(const sals_config* cfg, const void* U, const void* q,
+                                const void* latent_cache, const void* v_cache, int64_t cap,
+                                int32_t batch, const int32_t* d_seq_len, int32_t max_seq_len,
+                                void* out, void* workspace, size_t ws_bytes, int32_t iters,
+                                float* stage_ms, void* stream);
+
+/*
  * Dense full-KV comparator built in the same library (the "vs dense" baseline
  * of the north star; FlashAttention-2 is the paper's).
  * sals_dense_append: k_cache[b, pos] = RoPE_pos(k_new[b]) (post-RoPE cache),

@@ -18,6 +18,21 @@ namespace {
 thread_local std::string g_err;
 std::atomic<uint64_t> g_launches{0};
 
+// Optional per-stage event recorder (sals_decode_profile only).
+enum { kStQproj = 0, kStScore, kStTopk, kStReconAttn, kStFlash, kStMerge, kNumStages };
+struct StageTimer {
+  cudaEvent_t ev[kNumStages + 1];
+  float ms[kNumStages];
+  bool used[kNumStages];
+};
+thread_local StageTimer* g_timer = nullptr;
+void mark_begin(cudaStream_t st) { if (g_timer) cudaEventRecord(g_timer->ev[kNumStages], st); }
+void mark(int stage, cudaStream_t st) {
+  if (!g_timer) return;
+  cudaEventRecord(g_timer->ev[stage], st);
+  g_timer->used[stage] = true;
+}
+
 sals_status fail(sals_status s, const char* fmt, ...) {
   char buf[512];
   va_list ap;
@@ -313,6 +328,7 @@ sals_status attend_list(const sals_config* c, const Plan& p, const void* U, cons
     sals_status s = launch_recon_attn_tc(t, batch, st);
     if (s != SALS_OK) return fail(s, "%s", tc_last_error());
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    mark(kStReconAttn, st);
   } else {
     ReconArgs r{};
     r.latent = latent; r.cap = cap; r.r = c->rank; r.U = U; r.sel = sel; r.count = count;
@@ -320,12 +336,14 @@ sals_status attend_list(const sals_config* c, const Plan& p, const void* U, cons
     r.rope = make_rope(c); r.kr = ws + p.off_kr;
     sals_status s = launch_recon_simt<T>(c, r, batch, p.kmax, st);
     if (s != SALS_OK) return s;
+    mark(kStReconAttn, st);
     FlashArgs f{};
     f.qrope = qrope; f.kbase = ws + p.off_kr; f.v_cache = v_cache; f.sel = sel; f.count = count;
     f.cap = cap; f.D = p.D; f.k_stride = c->top_k; f.n_q = c->num_q_heads; f.n_kv = c->num_kv_heads;
     f.nsplit = p.nsplit; f.chunk = p.chunk; f.scale_log2 = scale_log2(c); f.partials = part;
     s = launch_flash<T, false>(c, f, batch, st);
     if (s != SALS_OK) return s;
+    mark(kStFlash, st);
   }
   MergeArgs m{};
   m.partials = part;
@@ -334,8 +352,9 @@ sals_status attend_list(const sals_config* c, const Plan& p, const void* U, cons
   m.nsplit = p.nsplit; m.n_q = c->num_q_heads; m.head_dim = c->head_dim;
   m.out = partial_out ? (void*)partial_out : out;
   m.normalize = partial_out ? 0 : 1;
-  if (partial_out) return launch_merge<float>(c, m, batch, st);
-  return launch_merge<T>(c, m, batch, st);
+  sals_status ms = partial_out ? launch_merge<float>(c, m, batch, st) : launch_merge<T>(c, m, batch, st);
+  mark(kStMerge, st);
+  return ms;
 }
 
 template <typename T>
@@ -354,14 +373,17 @@ sals_status decode_impl(const sals_config* c, const void* U, const void* q, cons
   pa.U = U; pa.x = q; pa.x_stride = c->num_q_heads * c->head_dim; pa.D = p.D; pa.r = c->rank;
   pa.ncols = c->score_rank; pa.B = batch; pa.head_dim = c->head_dim; pa.group = p.G;
   pa.n_q = c->num_q_heads; pa.out_f32 = qtil; pa.qrope = qrope; pa.seq_len = seq_len; pa.rope = make_rope(c);
+  mark_begin(st);
   sals_status s = launch_project<T>(c, p, true, pa, c->score_rank, st);
   if (s != SALS_OK) return s;
+  mark(kStQproj, st);
 
   ScoreArgs sa{};
   sa.latent = latent; sa.cap = cap; sa.r = c->rank; sa.rstar = c->score_rank; sa.qtil = qtil;
   sa.len = seq_len; sa.scores = scores; sa.stride = sstride;
   s = launch_score<T>(c, sa, batch, max_s, st);
   if (s != SALS_OK) return s;
+  mark(kStScore, st);
 
   TopkArgs ta{};
   ta.scores = scores; ta.score_stride = sstride; ta.seq_len = seq_len; ta.idx_base = 0;
@@ -370,6 +392,7 @@ sals_status decode_impl(const sals_config* c, const void* U, const void* q, cons
   ta.sel_out2 = sel_out;
   s = launch_topk(ta, batch, p.tk_cs, p.tk_smem, st);
   if (s != SALS_OK) return s;
+  mark(kStTopk, st);
 
   return attend_list<T>(c, p, U, latent, v_cache, cap, batch, 0, sel, count, ws, out, nullptr, st);
 }
@@ -447,6 +470,36 @@ sals_status sals_decode(const sals_config* cfg, const void* U, const void* q, co
                                       sel_idx_out, scores_out, ws, p, st);
   return decode_impl<float>(cfg, U, q, latent_cache, v_cache, cap, batch, d_seq_len, max_seq_len, out,
                             sel_idx_out, scores_out, ws, p, st);
+}
+
+sals_status sals_decode_profile(const sals_config* cfg, const void* U, const void* q, const void* latent_cache,
+                                const void* v_cache, int64_t cap, int32_t batch, const int32_t* d_seq_len,
+                                int32_t max_seq_len, void* out, void* workspace, size_t ws_bytes, int32_t iters,
+                                float* stage_ms, void* stream) {
+  if (!stage_ms || iters < 1) return fail(SALS_ERR_INVALID_ARGUMENT, "stage_ms / iters");
+  StageTimer t{};
+  for (int i = 0; i <= kNumStages; ++i) SALS_CUDA_TRY(cudaEventCreate(&t.ev[i]));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  sals_status s = SALS_OK;
+  for (int it = 0; it < iters && s == SALS_OK; ++it) {
+    g_timer = &t;
+    s = sals_decode(cfg, U, q, latent_cache, v_cache, cap, batch, d_seq_len, max_seq_len, out, nullptr, nullptr,
+                    workspace, ws_bytes, stream);
+    g_timer = nullptr;
+    if (s != SALS_OK) break;
+    if (cudaStreamSynchronize(st) != cudaSuccess) { s = fail(SALS_ERR_CUDA, "profile sync"); break; }
+    cudaEvent_t prev = t.ev[kNumStages];
+    for (int k = 0; k < kNumStages; ++k) {
+      if (!t.used[k]) continue;
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, prev, t.ev[k]);
+      t.ms[k] += ms;
+      prev = t.ev[k];
+    }
+  }
+  for (int k = 0; k < kNumStages; ++k) stage_ms[k] = t.used[k] ? t.ms[k] / iters : 0.f;
+  for (int i = 0; i <= kNumStages; ++i) cudaEventDestroy(t.ev[i]);
+  return s;
 }
 
 // ------------------------------------------------------------ dense baseline

@@ -20,7 +20,7 @@ SALS_PATH_AUTO, SALS_PATH_SIMT, SALS_PATH_TCGEN05 = 0, 1, 2
 STATUS = {0: "SALS_OK", 1: "SALS_ERR_INVALID_ARGUMENT", 2: "SALS_ERR_UNSUPPORTED",
           3: "SALS_ERR_WORKSPACE_TOO_SMALL", 4: "SALS_ERR_CUDA"}
 
-EXPORTED = ["sals_workspace_bytes", "sals_append_latent", "sals_decode", "sals_dense_append",
+EXPORTED = ["sals_workspace_bytes", "sals_append_latent", "sals_decode", "sals_decode_profile", "sals_dense_append",
             "sals_dense_workspace_bytes", "sals_dense_decode", "sals_shard_candidates", "sals_shard_attend",
             "sals_merge_partials", "sals_shard_workspace_bytes", "sals_status_string", "sals_last_error",
             "sals_launch_count"]
@@ -63,6 +63,7 @@ def _load():
         "sals_workspace_bytes": (SZ, [C, I32, I32]),
         "sals_append_latent": (I32, [C, P, P, P, I32, P, P, P, I64, P]),
         "sals_decode": (I32, [C, P, P, P, P, I64, I32, P, I32, P, P, P, P, SZ, P]),
+        "sals_decode_profile": (I32, [C, P, P, P, P, I64, I32, P, I32, P, P, SZ, I32, P, P]),
         "sals_dense_append": (I32, [C, P, P, I32, P, P, P, I64, P]),
         "sals_dense_workspace_bytes": (SZ, [C, I32, I32]),
         "sals_dense_decode": (I32, [C, P, P, P, I64, I32, P, I32, P, P, SZ, P]),
@@ -125,6 +126,18 @@ def sals_decode(cfg, U, q, latent_cache, v_cache, seq_len, max_seq_len, out, wor
     _check(_lib.sals_decode(ctypes.byref(cfg), _p(U), _p(q), _p(latent_cache), _p(v_cache), latent_cache.shape[1],
                             B, _p(seq_len), int(max_seq_len), _p(out), _p(sel_idx_out), _p(scores_out),
                             _p(workspace), workspace.numel(), _stream(stream)))
+
+
+STAGES = ["qproj_rope", "score", "topk", "recon_attn", "flash", "merge"]
+
+
+def sals_decode_profile(cfg, U, q, latent_cache, v_cache, seq_len, max_seq_len, out, workspace, iters=10,
+                        stream=None) -> dict:
+    ms = (ctypes.c_float * 6)()
+    _check(_lib.sals_decode_profile(ctypes.byref(cfg), _p(U), _p(q), _p(latent_cache), _p(v_cache),
+                                    latent_cache.shape[1], q.shape[0], _p(seq_len), int(max_seq_len), _p(out),
+                                    _p(workspace), workspace.numel(), int(iters), ms, _stream(stream)))
+    return {k: float(v) for k, v in zip(STAGES, ms)}
 
 
 def sals_dense_append(cfg, k_new, v_new, pos, k_cache, v_cache, stream=None):

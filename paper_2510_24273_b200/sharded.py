@@ -1,0 +1,163 @@
+"""Sequence-sharded SALS decode over P GPUs: one process per GPU,
+contiguous shards of every request's tokens, two all-gathers per layer.
+
+    rank p:  local q~, p' over its shard, local top-(k-x-z) candidates with
+             GLOBAL indices (sals_shard_candidates)
+    all-gather #1: (score, index) candidates -> [P, B, k]   (NCCL over NVLink)
+    rank p:  global TopK over the P*k candidates (identical on every rank),
+             reconstruct + RoPE + attention over the OWNED selected tokens
+             -> one (m, l, o) partial per (request, query head)   (sals_shard_attend)
+    all-gather #2: partials -> [P, B, n_q, d+2]
+    every rank: log-sum-exp merge -> y   (sals_merge_partials)
+
+The exchange plumbing (what is gathered, in which layout, and the merge order)
+lives in ``ShardedDecoder``; the device phases are injectable so the same
+orchestration runs on CPU with gloo and the fp64 oracle in the tests.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+
+def shard_bounds(seq_len: int, world: int, rank: int):
+    """Contiguous shard [start, end) of positions 0..seq_len-1 held by `rank`."""
+    per = math.ceil(seq_len / world)
+    start = min(rank * per, seq_len)
+    return start, min(start + per, seq_len)
+
+
+@dataclass
+class Phases:
+    """Device (or oracle) implementations of the three local phases."""
+    candidates: callable    # (latent_shard, start, local_len) -> (cand_score [B,k] f32, cand_idx [B,k] i32)
+    attend: callable        # (latent_shard, v_shard, start, local_len, all_score, all_idx) -> partial [B,n_q,d+2]
+    merge: callable         # (partial_all [P,B,n_q,d+2]) -> y [B, n_q*d]
+
+
+class ShardedDecoder:
+    def __init__(self, phases: Phases, group=None):
+        self.ph = phases
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def _gather(self, t: torch.Tensor) -> torch.Tensor:
+        """All-gather along a new leading rank axis ([P, *t.shape], rank order)."""
+        t = t.contiguous()
+        out = torch.empty((self.world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        dist.all_gather_into_tensor(out, t, group=self.group)
+        return out.view((self.world,) + tuple(t.shape))
+
+    def decode(self, latent_shard, v_shard, start, local_len):
+        cs, ci = self.ph.candidates(latent_shard, start, local_len)
+        all_s = self._gather(cs)            # [P, B, k], rank order = ascending global index
+        all_i = self._gather(ci)
+        part = self.ph.attend(latent_shard, v_shard, start, local_len, all_s, all_i)
+        part_all = self._gather(part)       # [P, B, n_q, d+2]
+        return self.ph.merge(part_all)
+
+
+def gpu_phases(cfg, U, q, seq_len, max_local_len, ws, world):
+    """Phases backed by the C ABI (libsals.so) on the current CUDA stream."""
+    from . import sals
+    B = q.shape[0]
+    k = cfg.top_k
+    n_q, d = cfg.num_q_heads, cfg.head_dim
+    cs = torch.empty(B, k, dtype=torch.float32, device=q.device)
+    ci = torch.empty(B, k, dtype=torch.int32, device=q.device)
+    part = torch.empty(B, n_q, d + 2, dtype=torch.float32, device=q.device)
+    out = torch.empty(B, n_q * d, dtype=q.dtype, device=q.device)
+
+    def candidates(lat, start, local_len):
+        sals.sals_shard_candidates(cfg, U, q, lat, start, local_len, max_local_len, seq_len, cs, ci, ws)
+        return cs, ci
+
+    def attend(lat, v, start, local_len, all_s, all_i):
+        sals.sals_shard_attend(cfg, U, q, lat, v, start, local_len, max_local_len, seq_len, all_s, all_i, world,
+                               part, ws)
+        return part
+
+    def merge(part_all):
+        sals.sals_merge_partials(cfg, part_all, world, B, out)
+        return out
+
+    return Phases(candidates, attend, merge)
+
+
+# ---------------------------------------------------------------------------
+# bench: c4 sequence-sharded over torchrun ranks (strong scaling)
+# ---------------------------------------------------------------------------
+def bench(args, rank, world):
+    import json
+    import time
+
+    import synth
+    from . import build, sals
+    build.build()
+    sys_shape = dict(synth.CONFIGS["c4"])
+    B, s, L = sys_shape["batch"], sys_shape["seq"], args.layers
+    cfg = sals.make_config(**sys_shape, path=args.path)
+    start, end = shard_bounds(s, world, rank)
+    n_loc = end - start
+    g = torch.Generator(device="cuda")
+    g.manual_seed(synth.SEED_BASE + 7)
+    layers = []
+    for _ in range(L):
+        ly = synth.gen_layer_torch(num_q_heads=sys_shape["num_q_heads"], num_kv_heads=sys_shape["num_kv_heads"],
+                                   head_dim=sys_shape["head_dim"], rank=sys_shape["rank"], batch=B, seq=n_loc,
+                                   generator=g)
+        layers.append(ly)
+    seq = torch.full((B,), s, dtype=torch.int32, device="cuda")
+    loc = torch.full((B,), n_loc, dtype=torch.int32, device="cuda")
+    ws = sals.alloc_workspace(sals.sals_shard_workspace_bytes(cfg, B, n_loc, world), "cuda")
+    owner = rank == world - 1                       # holds position s-1, appends the new token
+    pos_local = (loc - 1).to(torch.int32)
+    decs = [ShardedDecoder(gpu_phases(cfg, ly["U"], ly["q"], seq, n_loc, ws, world)) for ly in layers]
+
+    def step():
+        for ly, dec in zip(layers, decs):
+            if owner:
+                sals.sals_append_latent(cfg, ly["U"], ly["k_new"], ly["v_new"], pos_local, ly["latent"], ly["v"])
+            dec.decode(ly["latent"], ly["v"], start, loc)
+
+    stream = torch.cuda.Stream()
+    graph = None
+    with torch.cuda.stream(stream):
+        step()
+        stream.synchronize()
+        try:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream):
+                step()
+        except Exception:
+            graph = None
+        for _ in range(args.warmup):
+            graph.replay() if graph else step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            graph.replay() if graph else step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    if rank == 0:
+        line = {"metric": "decode attention tokens/s (32-layer attention step)", "value": B / (ms / 1e3),
+                "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic",
+                "config": {"workload": f"c4-sharded: B={B} n={s} sequence-sharded over {world} GPUs x{L} layers",
+                           "batch": B, "seq_len": s, "layers": L, "parallelism": f"sequence-shard x{world}",
+                           "graph": graph is not None},
+                "us_per_layer_step": ms * 1e3 / L}
+        print(json.dumps(line), flush=True)

@@ -96,3 +96,42 @@ CONFIGS = {
     "c5": dict(num_q_heads=32, num_kv_heads=32, head_dim=128, rank=512, score_rank=256, top_k=None,
                batch=None, seq=None, rope_base=10000.0, dtype="bf16"),
 }
+
+
+def gen_layer_torch(*, num_q_heads, num_kv_heads, head_dim, rank, batch, seq, cap=None, generator=None,
+                    device="cuda", dtype=None, dense=False):
+    """The same recipe as ``gen_problem`` drawn directly on the device with torch
+    (bench-sized problems: 32 layers x hundreds of MiB).  Returns a dict of
+    device tensors; ``dense`` adds a full pre-RoPE key cache K for the dense
+    comparator."""
+    import torch
+    dtype = dtype or torch.bfloat16
+    g = generator
+    D = num_kv_heads * head_dim
+    G = num_q_heads // num_kv_heads
+    cap = cap or seq
+    U, _ = torch.linalg.qr(torch.randn(D, rank, device=device, generator=g, dtype=torch.float32))
+    sig = torch.tensor(spectrum(rank), device=device, dtype=torch.float32)
+    c = float(np.sqrt(D / float((sig ** 2).sum())))
+    latent = torch.randn(batch, cap, rank, device=device, generator=g, dtype=torch.float32) * (c * sig)
+    w = torch.randn(rank, device=device, generator=g) * sig
+    u = (U @ w).view(num_kv_heads, head_dim)
+    u = u / u.norm(dim=1, keepdim=True)
+    q = 0.8 * torch.randn(batch, num_q_heads, head_dim, device=device, generator=g)
+    q = q + 0.6 * float(np.sqrt(head_dim)) * u.repeat_interleave(G, dim=0)[None]
+    n = max(1, seq // 64)
+    pos = torch.randint(0, max(seq - 1, 1), (batch, n), device=device, generator=g)
+    amp = 3.0 * c * float(sig.norm())
+    latent.scatter_add_(1, pos[..., None].expand(batch, n, rank),
+                        (amp * w / w.norm()).expand(batch, n, rank).contiguous())
+    out = {
+        "U": U.to(dtype).contiguous(),
+        "latent": latent.to(dtype),
+        "v": torch.randn(batch, cap, D, device=device, generator=g, dtype=torch.float32).to(dtype),
+        "q": q.reshape(batch, num_q_heads * head_dim).to(dtype),
+        "k_new": torch.randn(batch, D, device=device, generator=g).to(dtype),
+        "v_new": torch.randn(batch, D, device=device, generator=g).to(dtype),
+    }
+    if dense:   # dense comparator's key cache: independent N(0,1) draws (timing only)
+        out["k_dense"] = torch.randn(batch, cap, D, device=device, generator=g, dtype=torch.float32).to(dtype)
+    return out
