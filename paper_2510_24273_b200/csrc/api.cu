@@ -114,7 +114,11 @@ RopeTable make_rope(const sals_config* c) {
   RopeTable t{};
   t.half = c->head_dim / 2;
   t.style = c->rope_style;
-  for (int p = 0; p < t.half; ++p) t.theta[p] = std::pow((double)c->rope_base, -2.0 * p / c->head_dim);
+  for (int p = 0; p < t.half; ++p) {
+    t.theta[p] = std::pow((double)c->rope_base, -2.0 * p / c->head_dim);
+    t.th_hi[p] = (float)t.theta[p];
+    t.th_lo[p] = (float)(t.theta[p] - (double)t.th_hi[p]);
+  }
   return t;
 }
 
@@ -129,7 +133,8 @@ size_t esize(const sals_config* c) { return c->dtype == SALS_BF16 ? 2 : 4; }
 struct Plan {
   int D, G, kmax;
   bool tc;                 // fused tcgen05 reconstruct + attention
-  int nsplit, chunk;       // flash split (SIMT) or 128-row tiles (tc)
+  int nsplit, chunk;       // flash split (SIMT) / 128-row tiles (tc v1) / chunks + tiles per CTA (tc v2)
+  bool tc2;
   int tk_cs, tk_slice;     // top-k cluster size / slice
   size_t tk_smem;
   int proj_cs, proj_rows;
@@ -180,7 +185,14 @@ sals_status make_plan(const sals_config* c, int batch, int max_s, Plan& p, bool 
   p.tc = want_tc && tc_eligible(c, batch, p.kmax);
   if (c->path == SALS_PATH_TCGEN05 && !p.tc && !for_size)
     return fail(SALS_ERR_UNSUPPORTED, "tcgen05 path needs bf16, B*k >= 128, d in {64,128,256}, D %% 256 == 0");
-  if (p.tc) {
+  p.tc2 = p.tc && tc2_supported(c->head_dim, p.D, c->rank, p.G);
+  if (p.tc2) {
+    const int ntiles = ceil_div(p.kmax, kTcRows);
+    const int64_t units = (int64_t)batch * (p.D / 256) * ntiles;
+    const int tpc = std::max(1, ceil_div(units, 148));
+    p.chunk = tpc;
+    p.nsplit = ceil_div(ntiles, tpc);
+  } else if (p.tc) {
     p.nsplit = ceil_div(p.kmax, kTcRows);
     p.chunk = kTcRows;
   } else {
@@ -210,7 +222,7 @@ template <typename T>
 sals_status launch_project(const sals_config* c, const Plan& p, bool pool, ProjectArgs& a, int ncols,
                            cudaStream_t st) {
   a.rows_per_cta = p.proj_rows;
-  const int ncolblk = ceil_div(ncols, 64);
+  const int ncolblk = ceil_div(ncols, 8 * (16 / (int)sizeof(T)));
   dim3 grid(p.proj_cs, ncolblk + (pool ? 1 : 0));
   static bool attr_done = false;
   if (!attr_done) {
@@ -218,8 +230,8 @@ sals_status launch_project(const sals_config* c, const Plan& p, bool pool, Proje
     SALS_CUDA_TRY(cudaFuncSetAttribute(project_kernel<T, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr_done = true;
   }
-  if (pool) SALS_CUDA_TRY(launch(project_kernel<T, true>, grid, dim3(128), 0, st, p.proj_cs, a));
-  else SALS_CUDA_TRY(launch(project_kernel<T, false>, grid, dim3(128), 0, st, p.proj_cs, a));
+  if (pool) SALS_CUDA_TRY(launch(project_kernel<T, true>, grid, dim3(kProjThreads), 0, st, p.proj_cs, a));
+  else SALS_CUDA_TRY(launch(project_kernel<T, false>, grid, dim3(kProjThreads), 0, st, p.proj_cs, a));
   return SALS_OK;
 }
 
@@ -250,7 +262,7 @@ sals_status launch_score(const sals_config* c, ScoreArgs a, int batch, int max_l
     case 324: k = latent_score_kernel<T, 32, 4>; break;
     default: return fail(SALS_ERR_UNSUPPORTED, "score rank layout");
   }
-  SALS_CUDA_TRY(launch(k, grid, dim3(256), 0, st, 0, a));
+  SALS_CUDA_TRY(launch(k, grid, dim3(kScoreThreads), 0, st, 0, a));
   return SALS_OK;
 }
 
@@ -261,7 +273,7 @@ sals_status launch_topk(const TopkArgs& a, int batch, int cs, size_t smem, cudaS
     SALS_CUDA_TRY(cudaFuncSetAttribute(topk_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr_done = true;
   }
-  SALS_CUDA_TRY(launch(topk_cluster_kernel, dim3(batch * cs), dim3(512), smem, st, cs, a));  // cluster attr even for cs == 1
+  SALS_CUDA_TRY(launch(topk_cluster_kernel, dim3(batch * cs), dim3(kTopkThreads), smem, st, cs, a));  // cluster attr even for cs == 1
   return SALS_OK;
 }
 
@@ -325,10 +337,14 @@ sals_status attend_list(const sals_config* c, const Plan& p, const void* U, cons
     t.sel = sel; t.count = count; t.k_stride = c->top_k; t.D = p.D; t.head_dim = c->head_dim;
     t.G = p.G; t.n_q = c->num_q_heads; t.pos_base = pos_base; t.rope = make_rope(c);
     t.qrope = qrope; t.scale_log2 = scale_log2(c); t.partials = part; t.ntiles = p.nsplit;
+    t.tiles_per_cta = p.tc2 ? p.chunk : 0;
+    const bool direct = p.tc2 && p.nsplit == 1 && !partial_out;
+    t.direct_out = direct ? out : nullptr;
     sals_status s = launch_recon_attn_tc(t, batch, st);
     if (s != SALS_OK) return fail(s, "%s", tc_last_error());
     g_launches.fetch_add(1, std::memory_order_relaxed);
     mark(kStReconAttn, st);
+    if (direct) return SALS_OK;   // y written by the fused kernel (single chunk per request)
   } else {
     ReconArgs r{};
     r.latent = latent; r.cap = cap; r.r = c->rank; r.U = U; r.sel = sel; r.count = count;
@@ -561,12 +577,12 @@ sals_status sals_dense_decode(const sals_config* cfg, const void* q, const void*
   m.partials = part; m.bh_stride = (int64_t)nsplit * (cfg->head_dim + 2); m.s_stride = cfg->head_dim + 2;
   m.nsplit = nsplit; m.n_q = cfg->num_q_heads; m.head_dim = cfg->head_dim; m.out = out; m.normalize = 1;
   if (cfg->dtype == SALS_BF16) {
-    SALS_CUDA_TRY(launch(project_kernel<__nv_bfloat16, true>, dim3(1, 1), dim3(128), 0, st, 1, pa));
+    SALS_CUDA_TRY(launch(project_kernel<__nv_bfloat16, true>, dim3(1, 1), dim3(kProjThreads), 0, st, 1, pa));
     s = launch_flash<__nv_bfloat16, true>(cfg, f, batch, st);
     if (s != SALS_OK) return s;
     return launch_merge<__nv_bfloat16>(cfg, m, batch, st);
   }
-  SALS_CUDA_TRY(launch(project_kernel<float, true>, dim3(1, 1), dim3(128), 0, st, 1, pa));
+  SALS_CUDA_TRY(launch(project_kernel<float, true>, dim3(1, 1), dim3(kProjThreads), 0, st, 1, pa));
   s = launch_flash<float, true>(cfg, f, batch, st);
   if (s != SALS_OK) return s;
   return launch_merge<float>(cfg, m, batch, st);

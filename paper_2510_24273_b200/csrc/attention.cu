@@ -78,7 +78,7 @@ recon_rope_simt_kernel(ReconArgs a) {
     const int row = rows[rr];
     if (row < 0) continue;
     int lo, hi; rope_pair(p, half, a.rope.style, lo, hi);
-    float c, s; rope_cs(a.rope.theta[p], a.pos_base + row, c, s);
+    float c, s; rope_cs_fast(a.rope.th_hi[p], a.rope.th_lo[p], (int)(a.pos_base + row), c, s);
     const float xl = Ks[rr * DH + lo], xh = Ks[rr * DH + hi];
     T* dst = kr + ((size_t)b * a.k_stride + t0 + rr) * a.D + g * DH;
     dst[lo] = Elem<T>::from_f(xl * c - xh * s);
@@ -240,23 +240,23 @@ __global__ void merge_kernel(MergeArgs a) {
   const int b = bh / a.n_q, h = bh % a.n_q;
   pdl_wait();
   const float* base = a.partials + (size_t)bh * a.bh_stride;
-  float M = -INFINITY;
-  for (int s = 0; s < a.nsplit; ++s) M = fmaxf(M, base[(size_t)s * a.s_stride]);
-  float L = 0.f;
-  for (int s = 0; s < a.nsplit; ++s) {
-    const float ms = base[(size_t)s * a.s_stride];
-    if (ms != -INFINITY) L += base[(size_t)s * a.s_stride + 1] * exp2f(ms - M);
-  }
-  const float invL = (L > 0.f) ? 1.f / L : 0.f;
   for (int i = threadIdx.x; i < a.head_dim; i += blockDim.x) {
-    float acc = 0.f;
+    // one pass over the splits with a running max (independent loads, no dependent phases)
+    float M = -INFINITY, L = 0.f, acc = 0.f;
+#pragma unroll 4
     for (int s = 0; s < a.nsplit; ++s) {
-      const float ms = base[(size_t)s * a.s_stride];
-      if (ms != -INFINITY) acc += base[(size_t)s * a.s_stride + 2 + i] * exp2f(ms - M);
+      const float* ps = base + (size_t)s * a.s_stride;
+      const float ms = ps[0], ls = ps[1], os = ps[2 + i];
+      if (ms == -INFINITY) continue;
+      const float Mn = fmaxf(M, ms);
+      const float c0 = exp2f(M - Mn), c1 = exp2f(ms - Mn);
+      L = L * c0 + ls * c1;
+      acc = acc * c0 + os * c1;
+      M = Mn;
     }
     if (a.normalize) {
       T* out = reinterpret_cast<T*>(a.out) + ((size_t)b * a.n_q + h) * a.head_dim;
-      out[i] = Elem<T>::from_f(acc * invL);
+      out[i] = Elem<T>::from_f(L > 0.f ? acc / L : 0.f);
     } else {   // un-normalised partial (M, L, O) for the cross-rank merge
       float* out = reinterpret_cast<float*>(a.out) + (size_t)bh * (a.head_dim + 2);
       out[2 + i] = acc;
@@ -284,7 +284,7 @@ __global__ void dense_append_kernel(DenseAppendArgs a) {
   for (int t = threadIdx.x; t < a.n_kv * half; t += blockDim.x) {
     const int g = t / half, p = t % half;
     int lo, hi; rope_pair(p, half, a.rope.style, lo, hi);
-    float c, s; rope_cs(a.rope.theta[p], pos, c, s);
+    float c, s; rope_cs_fast(a.rope.th_hi[p], a.rope.th_lo[p], (int)pos, c, s);
     const float xl = Elem<T>::to_f(k[g * a.head_dim + lo]), xh = Elem<T>::to_f(k[g * a.head_dim + hi]);
     kc[g * a.head_dim + lo] = Elem<T>::from_f(xl * c - xh * s);
     kc[g * a.head_dim + hi] = Elem<T>::from_f(xl * s + xh * c);

@@ -10,6 +10,11 @@
 
 namespace sals {
 
+// Block sizes shared by kernels and launcher.
+constexpr int kProjThreads = 256;
+constexpr int kScoreThreads = 256;
+constexpr int kTopkThreads = 512;
+
 struct ProjectArgs {
   const void* U;        // [D, r]
   const void* x;        // append: k_new [B, D]; qproj: q [B, n_q*d]

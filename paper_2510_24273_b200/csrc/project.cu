@@ -3,37 +3,32 @@
 //   qproj  (Alg. 1 line 2):           q~ = U[:, :r*]^T q_bar   (fp32)
 // plus (qproj launch only) RoPE of the query at position s_b - 1 (Alg. 1 line 7).
 //
-// Design: U [D, r] is read exactly once.  A thread-block cluster of CS CTAs
-// splits the D rows (the contraction axis); each CTA owns 64 output columns
-// (32 lanes x 2) and 4 warps that stride over its rows.  Partial sums are
-// reduced warp -> CTA in shared memory and CTA -> cluster through DSMEM in a
-// fixed order, so the result is deterministic and no global workspace or
-// atomic is needed.
+// Design: U [D, r] is read exactly once and the kernel is latency-bound (a few
+// MiB), so the goal is bytes in flight.  A thread-block cluster of CS CTAs
+// splits the D rows (the contraction axis); each CTA owns 8*EPC output columns
+// (8 lanes x one 16-byte vector) and its 8 warps stride over its rows four at a
+// time (lane / 8 = row slot), every lane keeping all its row loads in flight
+// before the FMAs.  Partials are reduced row-slot -> warp (shuffles) -> CTA
+// (shared memory, fixed warp order) -> cluster (DSMEM, fixed rank order), so
+// the result is deterministic and needs no global workspace or atomics.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace sals {
 
-constexpr int kProjThreads = 128;
-constexpr int kProjCols = 64;     // columns per CTA
+constexpr int kProjWarps = kProjThreads / 32;
 constexpr int kProjBT = 8;        // requests per pass
-constexpr int kProjMaxRows = 256; // rows per CTA (D / CS)
-
-template <typename T> __device__ __forceinline__ void load2(const T* p, float& a, float& b);
-template <> __device__ __forceinline__ void load2<float>(const float* p, float& a, float& b) {
-  float2 v = __ldg(reinterpret_cast<const float2*>(p)); a = v.x; b = v.y;
-}
-template <> __device__ __forceinline__ void load2<__nv_bfloat16>(const __nv_bfloat16* p, float& a, float& b) {
-  uint32_t v = __ldg(reinterpret_cast<const unsigned int*>(p));
-  a = __uint_as_float(v << 16); b = __uint_as_float(v & 0xffff0000u);
-}
+constexpr int kProjMaxRows = 512; // rows per CTA (D / CS)
+constexpr int kProjUnroll = 8;    // row loads in flight per lane
 
 template <typename T, bool POOL>
 __global__ void __launch_bounds__(kProjThreads)
 project_kernel(ProjectArgs a) {
+  constexpr int EPC = Elem<T>::kPer16;       // columns per lane
+  constexpr int CPB = 8 * EPC;               // columns per CTA
   __shared__ float xs[kProjBT][kProjMaxRows];
-  __shared__ float wred[4][kProjBT][kProjCols];
-  __shared__ float cred[kProjBT][kProjCols];
+  __shared__ float wred[kProjWarps][kProjBT][CPB];
+  __shared__ float cred[kProjBT][CPB];
   const int CS = (int)cluster_nctarank();
   const int rank = (int)cluster_ctarank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -47,11 +42,11 @@ project_kernel(ProjectArgs a) {
     const int half = a.rope.half, d = 2 * half;
     const int nq = a.n_q;
     for (int b = rank; b < a.B; b += CS) {
-      const int64_t pos = (int64_t)a.seq_len[b] - 1;
+      const int pos = a.seq_len[b] - 1;
       for (int t = tid; t < half * nq; t += kProjThreads) {
         const int p = t % half, h = t / half;
         int lo, hi; rope_pair(p, half, a.rope.style, lo, hi);
-        float c, s; rope_cs(a.rope.theta[p], pos, c, s);
+        float c, s; rope_cs_fast(a.rope.th_hi[p], a.rope.th_lo[p], pos, c, s);
         const float xl = Elem<T>::to_f(x[(size_t)b * a.x_stride + h * d + lo]);
         const float xh = Elem<T>::to_f(x[(size_t)b * a.x_stride + h * d + hi]);
         a.qrope[((size_t)b * nq + h) * d + lo] = xl * c - xh * s;
@@ -78,8 +73,12 @@ project_kernel(ProjectArgs a) {
   const int rows_per = a.rows_per_cta;
   const int row0 = rank * rows_per;
   const int row1 = min(a.D, row0 + rows_per);
-  const int col = blockIdx.y * kProjCols + 2 * lane;
+  const int slot = lane >> 3;                       // row slot 0..3 within a warp step
+  const int cl = lane & 7;                          // column vector within the CTA's block
+  const int col = blockIdx.y * CPB + cl * EPC;
   const bool col_ok = col < a.ncols;
+  const char* Ub = reinterpret_cast<const char*>(U);
+  const size_t row_bytes = (size_t)a.r * sizeof(T);
 
   for (int b0 = 0; b0 < a.B; b0 += kProjBT) {
     const int nb = min(kProjBT, a.B - b0);
@@ -100,53 +99,68 @@ project_kernel(ProjectArgs a) {
     }
     __syncthreads();
 
-    float acc[kProjBT][2];
+    float acc[kProjBT][EPC];
 #pragma unroll
-    for (int bb = 0; bb < kProjBT; ++bb) acc[bb][0] = acc[bb][1] = 0.f;
+    for (int bb = 0; bb < kProjBT; ++bb)
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) acc[bb][e] = 0.f;
     if (col_ok) {
-      int c = row0 + warp;
-#pragma unroll 1
-      for (; c + 12 < row1; c += 16) {
-        float u[4][2];
+      // rows handled by this lane: row0 + 4*(warp + 8*i) + slot
+      for (int base = row0 + 4 * warp + slot; base < row1; base += 4 * kProjWarps * kProjUnroll) {
+        uint4 raw[kProjUnroll];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) load2<T>(U + (size_t)(c + 4 * q) * a.r + col, u[q][0], u[q][1]);
+        for (int u = 0; u < kProjUnroll; ++u) {
+          const int c = base + u * 4 * kProjWarps;
+          raw[u] = (c < row1) ? ld_nc_v4(Ub + (size_t)c * row_bytes + col * sizeof(T)) : make_uint4(0, 0, 0, 0);
+        }
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int u = 0; u < kProjUnroll; ++u) {
+          const int c = base + u * 4 * kProjWarps;
+          if (c < row1) {
+            float uf[EPC];
+            Elem<T>::unpack(raw[u], uf);
 #pragma unroll
-          for (int bb = 0; bb < kProjBT; ++bb) {
-            const float xv = xs[bb][c + 4 * q - row0];
-            acc[bb][0] = fmaf(u[q][0], xv, acc[bb][0]);
-            acc[bb][1] = fmaf(u[q][1], xv, acc[bb][1]);
+            for (int bb = 0; bb < kProjBT; ++bb) {
+              const float xv = xs[bb][c - row0];
+#pragma unroll
+              for (int e = 0; e < EPC; ++e) acc[bb][e] = fmaf(uf[e], xv, acc[bb][e]);
+            }
           }
-      }
-      for (; c < row1; c += 4) {
-        float u0, u1; load2<T>(U + (size_t)c * a.r + col, u0, u1);
-#pragma unroll
-        for (int bb = 0; bb < kProjBT; ++bb) {
-          const float xv = xs[bb][c - row0];
-          acc[bb][0] = fmaf(u0, xv, acc[bb][0]);
-          acc[bb][1] = fmaf(u1, xv, acc[bb][1]);
         }
       }
     }
+    // reduce the 4 row slots of the warp (lanes cl, cl+8, cl+16, cl+24)
 #pragma unroll
-    for (int bb = 0; bb < kProjBT; ++bb) {
-      wred[warp][bb][2 * lane] = acc[bb][0];
-      wred[warp][bb][2 * lane + 1] = acc[bb][1];
+    for (int bb = 0; bb < kProjBT; ++bb)
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) {
+        float v = acc[bb][e];
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        acc[bb][e] = v;
+      }
+    if (slot == 0) {
+#pragma unroll
+      for (int bb = 0; bb < kProjBT; ++bb)
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) wred[warp][bb][cl * EPC + e] = acc[bb][e];
     }
     __syncthreads();
-    for (int i = tid; i < kProjBT * kProjCols; i += kProjThreads) {
-      const int bb = i / kProjCols, j = i % kProjCols;
-      cred[bb][j] = ((wred[0][bb][j] + wred[1][bb][j]) + wred[2][bb][j]) + wred[3][bb][j];
+    for (int i = tid; i < kProjBT * CPB; i += kProjThreads) {
+      const int bb = i / CPB, j = i % CPB;
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < kProjWarps; ++w) s += wred[w][bb][j];
+      cred[bb][j] = s;
     }
     cluster_sync_all();
     // each rank reduces a 1/CS share of the outputs over ranks 0..CS-1 (fixed order)
-    const int nout = nb * kProjCols;
+    const int nout = nb * CPB;
     const int share = (nout + CS - 1) / CS;
     const uint32_t cred_addr = smem_u32(&cred[0][0]);
     for (int o = rank * share + tid; o < min(nout, (rank + 1) * share); o += kProjThreads) {
-      const int bb = o / kProjCols, j = o % kProjCols;
-      const int cj = blockIdx.y * kProjCols + j;
+      const int bb = o / CPB, j = o % CPB;
+      const int cj = blockIdx.y * CPB + j;
       float sum = 0.f;
       for (int c = 0; c < CS; ++c) sum += ld_dsmem_f32(mapa_shared(cred_addr + o * 4, c));
       if (cj < a.ncols) {

@@ -257,7 +257,7 @@ recon_attn_tc_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_co
     for (int p0 = 0; p0 < HALF; p0 += PCH) {
       float cs[PCH], sn[PCH];
 #pragma unroll
-      for (int i = 0; i < PCH; ++i) rope_cs(a.rope.theta[p0 + i], pos, cs[i], sn[i]);
+      for (int i = 0; i < PCH; ++i) rope_cs_fast(a.rope.th_hi[p0 + i], a.rope.th_lo[p0 + i], (int)pos, cs[i], sn[i]);
 #pragma unroll
       for (int j = 0; j < HPB; ++j) {
         float xl[PCH], xh[PCH];
@@ -413,6 +413,8 @@ cudaError_t launch_g(const CUtensorMap& map, const TcArgs& a, int batch, cudaStr
 
 }  // namespace
 
+cudaError_t launch_recon_attn_tc2(const CUtensorMap& map, const TcArgs& a, int batch, cudaStream_t st);
+
 bool tc_supported(int head_dim, int D, int rank, int G) {
   return (head_dim == 64 || head_dim == 128 || head_dim == 256) && D % kBN == 0 && rank % kBK == 0 &&
          (G == 1 || G == 2 || G == 4 || G == 8) && !(head_dim == 64 && G == 8);
@@ -434,6 +436,11 @@ sals_status launch_recon_attn_tc(const TcArgs& a, int batch, cudaStream_t st) {
   if (cr != CUDA_SUCCESS) { g_tc_err = "cuTensorMapEncodeTiled failed (U must be 16-B aligned)"; return SALS_ERR_CUDA; }
   cudaError_t e;
   const int style = a.rope.style;
+  if (a.tiles_per_cta > 0) {   // planned for the persistent v2 kernel
+    e = launch_recon_attn_tc2(map, a, batch, st);
+    if (e != cudaSuccess) { g_tc_err = cudaGetErrorString(e); return SALS_ERR_CUDA; }
+    return SALS_OK;
+  }
   switch (a.head_dim) {
     case 64: e = style ? launch_g<64, 1>(map, a, batch, st) : launch_g<64, 0>(map, a, batch, st); break;
     case 128: e = style ? launch_g<128, 1>(map, a, batch, st) : launch_g<128, 0>(map, a, batch, st); break;

@@ -18,10 +18,13 @@ struct TcArgs {
   const float* qrope;
   float scale_log2;
   float* partials;        // [B, n_q, ntiles, d+2]
-  int ntiles;             // tiles per request = ceil(k / 128)
+  int ntiles;             // v1: tiles per request = ceil(k / 128); v2: chunks per request
+  int tiles_per_cta;      // v2: tiles of 128 tokens per CTA (chunk length)
+  void* direct_out;       // v2 with one chunk: write y [B, n_q*d] directly (no merge kernel)
 };
 
 bool tc_supported(int head_dim, int D, int rank, int G);
+bool tc2_supported(int head_dim, int D, int rank, int G);   // persistent v2 (d = 128, G <= 4)
 sals_status launch_recon_attn_tc(const TcArgs& a, int batch, cudaStream_t st);
 const char* tc_last_error();
 

@@ -1,0 +1,444 @@
+// Path T v2: persistent, warp-specialised fused reconstruction + RoPE + sparse
+// attention (Alg. 1 lines 6-9; Eq. 6) for head_dim 128.
+//
+// One CTA per (request b, 256-column block = 2 KV heads, chunk of up to
+// `tpc` tiles of 128 selected tokens).  The CTA streams its tiles:
+//   warp 0      : U tiles (B operand) by TMA, 3-stage mbarrier ring
+//   warps 4-7   : gathered latent rows (A operand) by cp.async into SWIZZLE_128B
+//   warp 1      : TMEM allocation + the single tcgen05.mma issuer; the 128 x 256
+//                 fp32 accumulator is DOUBLE-BUFFERED in TMEM (2 x 256 columns),
+//                 so the MMA of tile i+1 runs while tile i is in the epilogue
+//   warp 2      : the tile's V rows (512 contiguous bytes each) by cp.async.bulk
+//   warps 8-15  : epilogue.  Warp w reads TMEM lanes 32 (w % 4).. (its 32
+//                 tokens); half h = (w-8)/4 rotates pairs [32h, 32h+32) of both
+//                 KV heads at each token's original position and forms partial
+//                 logits for the G query heads of each; the halves exchange
+//                 partial logits through shared memory, then half h owns KV
+//                 head h: tile max / sum, online-softmax rescale, P V over the
+//                 staged V rows.  Logits and K_C never leave the SM.
+// After its last tile the CTA writes y directly (single chunk) or one
+// (m, l, o) partial per (query head, chunk) for merge_kernel.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "recon_attn_tc.h"
+
+namespace sals {
+namespace tc2 {
+
+constexpr int kRows = 128, kBK = 64, kBN = 256, kStages = 3, kDH = 128;
+constexpr int kThreads = 512;
+constexpr int kABytes = kRows * kBK * 2;   // 16 KB
+constexpr int kBBytes = kBN * kBK * 2;     // 32 KB
+constexpr int kVBytes = kRows * kBN * 2;   // 64 KB
+
+__host__ __device__ constexpr int smem_bytes(int G) {
+  return 1024 + kStages * (kABytes + kBBytes) + kVBytes + 2 * G * 64 * 8 /*sQ*/ + 2 * 2 * G * kRows * 4 /*sL*/ +
+         2 * G * kRows * 4 /*sP*/ + 1024 /*misc*/;
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void cp_async_16(uint32_t dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void bar_epi() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void bar_half(int h) { asm volatile("bar.sync %0, 128;" ::"r"(2 + h) : "memory"); }
+
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kBN >> 3) << 17) |
+                            ((uint32_t)(kRows >> 4) << 24);
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct KArgs {
+  TcArgs a;
+};
+
+template <int G, int STYLE>
+__global__ void __launch_bounds__(kThreads, 1)
+recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_constant__ KArgs ka) {
+  constexpr int NQH = 2 * G;             // query heads of this CTA (2 KV heads)
+  const TcArgs& a = ka.a;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + kStages * kABytes;
+  uint8_t* sV = sB + kStages * kBBytes;
+  float2* sQ = reinterpret_cast<float2*>(sV + kVBytes);          // [NQH][64] (q_lo, q_hi) per pair
+  float* sL = reinterpret_cast<float*>(sQ + NQH * 64);           // [2 halves][NQH][128] partial logits
+  float* sP = sL + 2 * NQH * kRows;                              // [NQH][128] probabilities
+  float* sRed = sP + NQH * kRows;                                // [2 kinds][2 halves][4][G]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sRed + 2 * 2 * 4 * G + (G & 1 ? 0 : 0));
+  uint64_t* full = bars;                 // [stages]
+  uint64_t* empty = bars + kStages;      // [stages]
+  uint64_t* tfull = bars + 2 * kStages;  // [2]
+  uint64_t* tempty = tfull + 2;          // [2]
+  uint64_t* vfull = tempty + 2;
+  uint64_t* vempty = vfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(vempty + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int chunk = blockIdx.x, nb = blockIdx.y, b = blockIdx.z;
+  const int n0 = nb * kBN;
+
+  pdl_wait();
+  const int cnt = a.count[b];
+  const int ntiles_b = (cnt + kRows - 1) / kRows;
+  const int t_begin = chunk * a.tiles_per_cta;
+  const int t_end = min(ntiles_b, t_begin + a.tiles_per_cta);
+  const int ntile = max(0, t_end - t_begin);
+  const int* selb = a.sel + (size_t)b * a.k_stride;
+
+  if (ntile == 0) {   // no selected tokens for this chunk: empty partials
+    if (tid < NQH) {
+      const int h = nb * NQH + tid;
+      float* dst = a.partials + (((size_t)b * a.n_q + h) * a.ntiles + chunk) * (kDH + 2);
+      dst[0] = -INFINITY;
+      dst[1] = 0.f;
+    }
+    pdl_launch_dependents();
+    return;
+  }
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 128 + 1); mbar_init(&empty[s], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8); }
+    mbar_init(vfull, 1);
+    mbar_init(vempty, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (warp >= 8) {   // rotated, scaled queries: sQ[qh][p] = (q[lo(p)], q[hi(p)])
+    for (int i = tid - 256; i < NQH * 64; i += 256) {
+      const int qh = i >> 6, p = i & 63;
+      const int lo = STYLE == 0 ? p : 2 * p, hi = STYLE == 0 ? p + 64 : 2 * p + 1;
+      const float* qr = a.qrope + ((size_t)b * a.n_q + nb * NQH + qh) * kDH;
+      sQ[i] = make_float2(qr[lo] * a.scale_log2, qr[hi] * a.scale_log2);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int nk = a.r / kBK;
+
+  if (warp == 0) {
+    // ================= U (B operand) producer =================
+    if (lane == 0) {
+      int u = 0;
+      for (int it = 0; it < ntile; ++it)
+        for (int kc = 0; kc < nk; ++kc, ++u) {
+          const int s = u % kStages;
+          if (u >= kStages) mbar_wait(&empty[s], ((u / kStages) - 1) & 1);
+          mbar_arrive_expect_tx(&full[s], kBBytes);
+          tma_load_2d(smem_u32(sB + s * kBBytes), &tmap_u, kc * kBK, n0, &full[s]);
+        }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer =================
+    if (lane == 0) {
+      int u = 0;
+      for (int it = 0; it < ntile; ++it) {
+        const int buf = it & 1;
+        if (it >= 2) mbar_wait(&tempty[buf], ((it >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t acc = tmem + buf * kBN;
+        for (int kc = 0; kc < nk; ++kc, ++u) {
+          const int s = u % kStages;
+          mbar_wait(&full[s], (u / kStages) & 1);
+          tc_fence_after();
+          fence_proxy_async();
+          const uint32_t ab = smem_u32(sA + s * kABytes), bb = smem_u32(sB + s * kBBytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            mma_bf16(acc, sw128_desc(ab + k * 32), sw128_desc(bb + k * 32), (kc | k) ? 1u : 0u);
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&tfull[buf]);
+      }
+    }
+  } else if (warp == 2) {
+    // ================= V rows producer =================
+    if (lane == 0) {
+      const char* vb = reinterpret_cast<const char*>(a.v_cache);
+      for (int it = 0; it < ntile; ++it) {
+        const int tile = t_begin + it;
+        const int nv = min(kRows, cnt - tile * kRows);
+        if (it >= 1) mbar_wait(vempty, (it - 1) & 1);
+        mbar_arrive_expect_tx(vfull, (uint32_t)nv * (kBN * 2));
+        for (int t = 0; t < nv; ++t) {
+          const int row = selb[tile * kRows + t];
+          bulk_load(smem_u32(sV + t * (kBN * 2)), vb + (((size_t)b * a.cap + row) * a.D + n0) * 2, kBN * 2, vfull);
+        }
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ================= A producers: gathered latent rows =================
+    const char* latent = reinterpret_cast<const char*>(a.latent);
+    const int aw = warp - 4, ch = lane & 7;
+    int u = 0;
+    for (int it = 0; it < ntile; ++it) {
+      const int tile = t_begin + it;
+      const int nv = min(kRows, cnt - tile * kRows);
+      int rows[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int rl = aw * 32 + i * 4 + (lane >> 3);
+        rows[i] = rl < nv ? selb[tile * kRows + rl] : -1;
+      }
+      for (int kc = 0; kc < nk; ++kc, ++u) {
+        const int s = u % kStages;
+        if (u >= kStages) mbar_wait(&empty[s], ((u / kStages) - 1) & 1);
+        const uint32_t base = smem_u32(sA + s * kABytes);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int rl = aw * 32 + i * 4 + (lane >> 3);
+          const int row = rows[i];
+          const char* src = latent + (((size_t)b * a.cap + (row >= 0 ? row : 0)) * a.r + kc * kBK + ch * 8) * 2;
+          cp_async_16(base + rl * 128 + ((ch ^ (rl & 7)) << 4), src, row >= 0 ? 16u : 0u);
+        }
+        cp_async_arrive_noinc(&full[s]);
+      }
+    }
+  } else if (warp >= 8) {
+    // ================= epilogue =================
+    const int ew = warp - 8, rq = warp & 3, hf = ew >> 2;
+    const int m = rq * 32 + lane;                  // token row of the tile (TMEM lane)
+    const int n = rq * 32 + lane;                  // dim of KV head hf owned in P V
+    float m_run[G], l_run[G], o[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) { m_run[g] = -INFINITY; l_run[g] = 0.f; o[g] = 0.f; }
+    const uint32_t tl = tmem + ((uint32_t)(rq * 32) << 16);
+    for (int it = 0; it < ntile; ++it) {
+      const int tile = t_begin + it, buf = it & 1;
+      const int nv = min(kRows, cnt - tile * kRows);
+      const int row = m < nv ? selb[tile * kRows + m] : -1;
+      const int pos = (int)a.pos_base + (row >= 0 ? row : 0);
+      mbar_wait(&tfull[buf], (it >> 1) & 1);
+      tc_fence_after();
+      float part[2][G];
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int g = 0; g < G; ++g) part[j][g] = 0.f;
+      const uint32_t tacc = tl + buf * kBN;
+#pragma unroll 1
+      for (int pc = 0; pc < 2; ++pc) {
+        const int p0 = 32 * hf + 16 * pc;
+        float cs[16], sn[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) rope_cs_fast(a.rope.th_hi[p0 + i], a.rope.th_lo[p0 + i], pos, cs[i], sn[i]);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          float xl[16], xh[16];
+          if (STYLE == 0) {
+            tmem_ld16(tacc + j * kDH + p0, xl);
+            tmem_ld16(tacc + j * kDH + 64 + p0, xh);
+          } else {
+            float t0[16], t1[16];
+            tmem_ld16(tacc + j * kDH + 2 * p0, t0);
+            tmem_ld16(tacc + j * kDH + 2 * p0 + 16, t1);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              xl[i] = t0[2 * i]; xh[i] = t0[2 * i + 1];
+              xl[8 + i] = t1[2 * i]; xh[8 + i] = t1[2 * i + 1];
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float rl = xl[i] * cs[i] - xh[i] * sn[i];
+            const float rh = xl[i] * sn[i] + xh[i] * cs[i];
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              const float2 q = sQ[(j * G + g) * 64 + p0 + i];
+              part[j][g] = fmaf(q.x, rl, fmaf(q.y, rh, part[j][g]));
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);     // this warp is done with the accumulator
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int g = 0; g < G; ++g) sL[(hf * NQH + j * G + g) * kRows + m] = part[j][g];
+      bar_epi();
+      // ---- half hf owns KV head hf: full logits, tile softmax, online rescale
+      float lg[G], mnew[G], alpha[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const int q = hf * G + g;
+        lg[g] = (row >= 0) ? sL[q * kRows + m] + sL[(NQH + q) * kRows + m] : -INFINITY;
+        float v = lg[g];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
+        if (lane == 0) sRed[(hf * 4 + rq) * G + g] = v;
+      }
+      bar_half(hf);
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const float* r = sRed + hf * 4 * G + g;
+        const float mt = fmaxf(fmaxf(r[0], r[G]), fmaxf(r[2 * G], r[3 * G]));
+        mnew[g] = fmaxf(m_run[g], mt);
+        alpha[g] = exp2f(m_run[g] - mnew[g]);        // m_run = -inf -> 0
+        const float p = (row >= 0) ? exp2f(lg[g] - mnew[g]) : 0.f;
+        sP[(hf * G + g) * kRows + m] = p;
+        float v = p;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if (lane == 0) sRed[2 * 4 * G + (hf * 4 + rq) * G + g] = v;
+      }
+      bar_half(hf);
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const float* r = sRed + 2 * 4 * G + hf * 4 * G + g;
+        const float lt = (r[0] + r[G]) + (r[2 * G] + r[3 * G]);
+        l_run[g] = l_run[g] * alpha[g] + lt;
+        m_run[g] = mnew[g];
+        o[g] *= alpha[g];
+      }
+      mbar_wait(vfull, it & 1);
+      // ---- P V over the staged rows: dim n of KV head hf
+      const unsigned short* vcol = reinterpret_cast<const unsigned short*>(sV) + hf * kDH + n;
+      const float* pp = sP + hf * G * kRows;
+#pragma unroll 4
+      for (int t = 0; t < nv; ++t) {
+        const float v = __uint_as_float((uint32_t)vcol[t * kBN] << 16);
+#pragma unroll
+        for (int g = 0; g < G; ++g) o[g] = fmaf(pp[g * kRows + t], v, o[g]);
+      }
+      bar_epi();                                       // sV / sP / sL / sRed free
+      if (ew == 0 && lane == 0) mbar_arrive(vempty);
+    }
+    // ---- write y (single chunk) or the chunk's partial
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int h = nb * NQH + hf * G + g;
+      if (a.direct_out) {
+        __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(a.direct_out) + ((size_t)b * a.n_q + h) * kDH;
+        y[n] = __float2bfloat16_rn(l_run[g] > 0.f ? o[g] / l_run[g] : 0.f);
+      } else {
+        float* dst = a.partials + (((size_t)b * a.n_q + h) * a.ntiles + chunk) * (kDH + 2);
+        dst[2 + n] = o[g];
+        if (n == 0) { dst[0] = m_run[g]; dst[1] = l_run[g]; }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+  pdl_launch_dependents();
+}
+
+template <int G, int STYLE>
+cudaError_t launch_t(const CUtensorMap& map, const TcArgs& a, int batch, cudaStream_t st) {
+  auto kern = recon_attn_tc2_kernel<G, STYLE>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(G));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.ntiles, a.D / kBN, batch);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem_bytes(G);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  KArgs ka{a};
+  return cudaLaunchKernelEx(&cfg, kern, map, ka);
+}
+
+}  // namespace tc2
+
+bool tc2_supported(int head_dim, int D, int rank, int G) {
+  return head_dim == 128 && D % tc2::kBN == 0 && rank % tc2::kBK == 0 && (G == 1 || G == 2 || G == 4);
+}
+
+cudaError_t launch_recon_attn_tc2(const CUtensorMap& map, const TcArgs& a, int batch, cudaStream_t st) {
+  const int style = a.rope.style;
+  switch (a.G) {
+    case 1: return style ? tc2::launch_t<1, 1>(map, a, batch, st) : tc2::launch_t<1, 0>(map, a, batch, st);
+    case 2: return style ? tc2::launch_t<2, 1>(map, a, batch, st) : tc2::launch_t<2, 0>(map, a, batch, st);
+    case 4: return style ? tc2::launch_t<4, 1>(map, a, batch, st) : tc2::launch_t<4, 0>(map, a, batch, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace sals

@@ -13,7 +13,6 @@
 
 namespace sals {
 
-constexpr int kScoreThreads = 256;
 
 template <typename T, int LG, int CPL>
 __global__ void __launch_bounds__(kScoreThreads)

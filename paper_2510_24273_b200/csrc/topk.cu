@@ -22,7 +22,6 @@
 
 namespace sals {
 
-constexpr int kTopkThreads = 512;
 constexpr int kTopkWarps = kTopkThreads / 32;
 
 // Inclusive scan of one value per thread across the 512-thread block.
@@ -63,7 +62,7 @@ topk_cluster_kernel(TopkArgs a) {
   const int CS = (int)cluster_nctarank();
   const int rank = (int)cluster_ctarank();
   const int b = blockIdx.x / CS;
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int slice = a.slice;
   uint32_t* keys = reinterpret_cast<uint32_t*>(tk_smem);
   uint8_t* cls = tk_smem + (size_t)slice * 4;   // 0 none, 1 forced, 2 ranked
@@ -122,39 +121,62 @@ topk_cluster_kernel(TopkArgs a) {
   } else if (need > 0) {
     uint32_t prefix = 0;
     int rem = need;
+    for (int i = tid; i < kTopkWarps * 256; i += kTopkThreads) (&whist[0][0])[i] = 0;
+    __syncthreads();
     for (int pass = 0; pass < 4; ++pass) {
       const int shift = 24 - 8 * pass;
-      for (int i = tid; i < kTopkWarps * 256; i += kTopkThreads) (&whist[0][0])[i] = 0;
-      __syncthreads();
-      for (int i = tid; i < nloc; i += kTopkThreads) {
-        if (cls[i] != 2) continue;
-        const uint32_t key = keys[i];
-        if (pass > 0 && ((key ^ prefix) >> (shift + 8)) != 0) continue;
-        atomicAdd(&whist[warp][(key >> shift) & 255u], 1u);
+      // per-warp histogram of the digit, warp-aggregated (few distinct digits per warp)
+      for (int base = warp * 32; base < nloc; base += kTopkThreads) {
+        const int i = base + lane;
+        bool ok = false;
+        uint32_t dg = 0;
+        if (i < nloc && cls[i] == 2) {
+          const uint32_t key = keys[i];
+          ok = (pass == 0) || (((key ^ prefix) >> (shift + 8)) == 0);
+          dg = (key >> shift) & 255u;
+        }
+        const uint32_t tag = ok ? dg : (256u + lane);
+        const uint32_t peers = __match_any_sync(0xffffffffu, tag);
+        if (ok && lane == __ffs(peers) - 1) atomicAdd(&whist[warp][dg], (uint32_t)__popc(peers));
       }
       __syncthreads();
       uint32_t* ch = chist[pass & 1];
       if (tid < 256) {
         uint32_t t = 0;
 #pragma unroll
-        for (int w = 0; w < kTopkWarps; ++w) t += whist[w][tid];
+        for (int w = 0; w < kTopkWarps; ++w) { t += whist[w][tid]; whist[w][tid] = 0; }
         ch[tid] = t;
       }
       cluster_sync_all();
-      // thread t (< 256) holds digit 255 - t; inclusive scan = count of digits >= it
-      int cnt = 0;
-      if (tid < 256) {
-        const uint32_t addr = smem_u32(&ch[255 - tid]);
-        for (int c = 0; c < CS; ++c) cnt += (int)ld_dsmem_u32(mapa_shared(addr, c));
+      if (warp == 0) {
+        // lane l owns digits 255 - 8l - j, j = 0..7 (descending); counts summed over the cluster
+        int c8[8], tot = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t addr = smem_u32(&ch[255 - 8 * lane - j]);
+          int v = 0;
+          for (int c = 0; c < CS; ++c) v += (int)ld_dsmem_u32(mapa_shared(addr, c));
+          c8[j] = v;
+          tot += v;
+        }
+        int incl = tot;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int nb = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= off) incl += nb;
+        }
+        int excl = incl - tot;
+        if (excl < rem && rem <= incl) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (excl < rem && rem <= excl + c8[j]) { s_digit = 255 - 8 * lane - j; s_need = rem - excl; }
+            excl += c8[j];
+          }
+        }
       }
-      if (tid == 0) { s_digit = 0; s_need = 0; }
-      const int incl = block_incl_scan(cnt, warp_tot);
-      const int excl = incl - cnt;
-      if (tid < 256 && excl < rem && rem <= incl) { s_digit = 255 - tid; s_need = rem - excl; }
       __syncthreads();
       prefix |= (uint32_t)s_digit << shift;
       rem = s_need;
-      __syncthreads();
     }
     T = prefix;
     need_eq = rem;
