@@ -112,7 +112,7 @@ sals_status sals_append_latent(const sals_config* cfg, const void* U, const void
  *   sel_idx_out  [B, k] int32 or NULL: C_b ascending, -1 padded past min(k, s_b)
  *   scores_out   [B, max_seq_len] fp32 or NULL: p' (debug / parity)
  *   workspace    >= sals_workspace_bytes(cfg, batch, max_seq_len) bytes, 256-B aligned
- * Limits (SALS_ERR_UNSUPPORTED): max_seq_len <= 524288, batch <= 65535,
+ * Limits (SALS_ERR_UNSUPPORTED): max_seq_len <= 393216, batch <= 65535,
  * n_q/n_kv <= 8.
  */
 sals_status sals_decode(const sals_config* cfg, const void* U, const void* q,

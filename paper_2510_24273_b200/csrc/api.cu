@@ -154,11 +154,11 @@ sals_status plan_topk(int n_entries, bool cand, Plan& p) {
   while (cs < 16 && ceil_div(n_entries, cs) > 2048) cs <<= 1;
   int slice = ceil_div(n_entries, cs);
   slice = (int)align_up(std::max(slice, 4), 4);
-  const int cap = cand ? 16384 : 32768;
+  const int cap = cand ? 16384 : 24576;
   if (slice > cap) return fail(SALS_ERR_UNSUPPORTED, "top-k over %d entries exceeds the cluster limit", n_entries);
   p.tk_cs = cs;
   p.tk_slice = slice;
-  p.tk_smem = (size_t)slice * 5 + 16 + (cand ? (size_t)slice * 4 : 0);
+  p.tk_smem = ((size_t)slice * 5 + 15) / 16 * 16 + (cand ? (size_t)slice * 4 : 0) + (size_t)(kTopkThreads / 32) * 256 * 4;
   return SALS_OK;
 }
 
@@ -269,7 +269,7 @@ sals_status launch_score(const sals_config* c, ScoreArgs a, int batch, int max_l
 sals_status launch_topk(const TopkArgs& a, int batch, int cs, size_t smem, cudaStream_t st) {
   static bool attr_done = false;
   if (!attr_done) {
-    SALS_CUDA_TRY(cudaFuncSetAttribute(topk_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    SALS_CUDA_TRY(cudaFuncSetAttribute(topk_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 180 * 1024));
     SALS_CUDA_TRY(cudaFuncSetAttribute(topk_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr_done = true;
   }
@@ -473,7 +473,7 @@ sals_status sals_decode(const sals_config* cfg, const void* U, const void* q, co
     return fail(SALS_ERR_INVALID_ARGUMENT, "NULL tensor argument");
   if (batch < 1 || batch > 65535) return fail(SALS_ERR_UNSUPPORTED, "batch %d outside [1, 65535]", batch);
   if (max_seq_len < 1 || max_seq_len > cap) return fail(SALS_ERR_INVALID_ARGUMENT, "need 1 <= max_seq_len <= cap");
-  if (max_seq_len > 524288) return fail(SALS_ERR_UNSUPPORTED, "max_seq_len > 524288");
+  if (max_seq_len > 393216) return fail(SALS_ERR_UNSUPPORTED, "max_seq_len > 393216");
   if (reinterpret_cast<uintptr_t>(workspace) % 256) return fail(SALS_ERR_INVALID_ARGUMENT, "workspace not 256-B aligned");
   Plan p{};
   s = make_plan(cfg, batch, max_seq_len, p, false);

@@ -29,6 +29,7 @@ project_kernel(ProjectArgs a) {
   __shared__ float xs[kProjBT][kProjMaxRows];
   __shared__ float wred[kProjWarps][kProjBT][CPB];
   __shared__ float cred[kProjBT][CPB];
+  __shared__ float incoming[kProjBT * CPB];   // [source rank][owned output] partials pushed by peers
   const int CS = (int)cluster_nctarank();
   const int rank = (int)cluster_ctarank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -41,16 +42,33 @@ project_kernel(ProjectArgs a) {
     // ---- role 2: RoPE of the query heads at position s_b - 1 (fp32 out) ----
     const int half = a.rope.half, d = 2 * half;
     const int nq = a.n_q;
-    for (int b = rank; b < a.B; b += CS) {
-      const int pos = a.seq_len[b] - 1;
-      for (int t = tid; t < half * nq; t += kProjThreads) {
-        const int p = t % half, h = t / half;
-        int lo, hi; rope_pair(p, half, a.rope.style, lo, hi);
-        float c, s; rope_cs_fast(a.rope.th_hi[p], a.rope.th_lo[p], pos, c, s);
-        const float xl = Elem<T>::to_f(x[(size_t)b * a.x_stride + h * d + lo]);
-        const float xh = Elem<T>::to_f(x[(size_t)b * a.x_stride + h * d + hi]);
-        a.qrope[((size_t)b * nq + h) * d + lo] = xl * c - xh * s;
-        a.qrope[((size_t)b * nq + h) * d + hi] = xl * s + xh * c;
+    // (request, head, pair) tasks split over the CS CTAs of this row; loads of 8
+    // tasks are issued before any math so the latency is paid once per batch
+    const int per_req = half * nq;
+    const int total = a.B * per_req;
+    for (int t0 = rank * kProjThreads + tid; t0 < total; t0 += CS * kProjThreads * 8) {
+      float xl[8], xh[8];
+      int lo_[8], hi_[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int t = t0 + u * CS * kProjThreads;
+        xl[u] = xh[u] = 0.f;
+        if (t < total) {
+          const int b = t / per_req, r = t % per_req, p = r % half, h = r / half;
+          rope_pair(p, half, a.rope.style, lo_[u], hi_[u]);
+          xl[u] = Elem<T>::to_f(x[(size_t)b * a.x_stride + h * d + lo_[u]]);
+          xh[u] = Elem<T>::to_f(x[(size_t)b * a.x_stride + h * d + hi_[u]]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int t = t0 + u * CS * kProjThreads;
+        if (t < total) {
+          const int b = t / per_req, r = t % per_req, p = r % half, h = r / half;
+          float c, s; rope_cs_fast(a.rope.th_hi[p], a.rope.th_lo[p], a.seq_len[b] - 1, c, s);
+          a.qrope[((size_t)b * nq + h) * d + lo_[u]] = xl[u] * c - xh[u] * s;
+          a.qrope[((size_t)b * nq + h) * d + hi_[u]] = xl[u] * s + xh[u] * c;
+        }
       }
     }
     pdl_launch_dependents();
@@ -153,16 +171,26 @@ project_kernel(ProjectArgs a) {
       for (int w = 0; w < kProjWarps; ++w) s += wred[w][bb][j];
       cred[bb][j] = s;
     }
-    cluster_sync_all();
-    // each rank reduces a 1/CS share of the outputs over ranks 0..CS-1 (fixed order)
+    __syncthreads();
+    // push every partial to the rank that owns its output (fire-and-forget DSMEM
+    // stores), then each rank sums the CS partials of its outputs in rank order
     const int nout = nb * CPB;
     const int share = (nout + CS - 1) / CS;
-    const uint32_t cred_addr = smem_u32(&cred[0][0]);
+    {
+      const uint32_t inc_addr = smem_u32(&incoming[0]);
+      for (int o = tid; o < nout; o += kProjThreads) {
+        const int owner = o / share, ol = o - owner * share;
+        st_dsmem_u32(mapa_shared(inc_addr + (rank * share + ol) * 4, owner),
+                     __float_as_uint(cred[o / CPB][o % CPB]));
+      }
+    }
+    cluster_sync_all();
     for (int o = rank * share + tid; o < min(nout, (rank + 1) * share); o += kProjThreads) {
       const int bb = o / CPB, j = o % CPB;
       const int cj = blockIdx.y * CPB + j;
+      const int ol = o - rank * share;
       float sum = 0.f;
-      for (int c = 0; c < CS; ++c) sum += ld_dsmem_f32(mapa_shared(cred_addr + o * 4, c));
+      for (int c = 0; c < CS; ++c) sum += incoming[c * share + ol];
       if (cj < a.ncols) {
         const int b = b0 + bb;
         if (POOL) {

@@ -134,7 +134,9 @@ recon_attn_tc_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_co
   constexpr int PCH = 32;                // rotation pairs per epilogue chunk
   const TcArgs& a = ka.a;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align with pointer arithmetic on the __shared__ array so the compiler keeps the shared
+  // address space (an integer round trip would turn every access into a generic load)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;                                       // [stages][128][128 B] swizzled
   uint8_t* sB = sA + kStages * kABytes;                     // [stages][256][128 B] swizzled
   uint8_t* sV = sB + kStages * kBBytes;                     // [128][512 B]
@@ -413,7 +415,8 @@ cudaError_t launch_g(const CUtensorMap& map, const TcArgs& a, int batch, cudaStr
 
 }  // namespace
 
-cudaError_t launch_recon_attn_tc2(const CUtensorMap& map, const TcArgs& a, int batch, cudaStream_t st);
+cudaError_t launch_recon_attn_tc2(const CUtensorMap& map, const CUtensorMap& ml, const CUtensorMap& mv,
+                                  const TcArgs& a, int batch, cudaStream_t st);
 
 bool tc_supported(int head_dim, int D, int rank, int G) {
   return (head_dim == 64 || head_dim == 128 || head_dim == 256) && D % kBN == 0 && rank % kBK == 0 &&
@@ -437,7 +440,25 @@ sals_status launch_recon_attn_tc(const TcArgs& a, int batch, cudaStream_t st) {
   cudaError_t e;
   const int style = a.rope.style;
   if (a.tiles_per_cta > 0) {   // planned for the persistent v2 kernel
-    e = launch_recon_attn_tc2(map, a, batch, st);
+    // gather4 maps: latent [B*cap, r] rows of 64-column boxes (SWIZZLE_128B) and
+    // V [B*cap, D] rows of 256-column boxes (linear), one row per box
+    CUtensorMap ml, mv;
+    const cuuint64_t rows = (cuuint64_t)batch * (cuuint64_t)a.cap;
+    if (rows > 0x7fffffffull) { g_tc_err = "B*cap exceeds the 2^31 rows of a TMA gather"; return SALS_ERR_UNSUPPORTED; }
+    cuuint64_t dl[2] = {(cuuint64_t)a.r, rows}, sl[1] = {(cuuint64_t)a.r * 2};
+    cuuint32_t bl[2] = {64, 1};
+    cuuint64_t dv[2] = {(cuuint64_t)a.D, rows}, sv[1] = {(cuuint64_t)a.D * 2};
+    cuuint32_t bv[2] = {256, 1};
+    if (g_encode(&ml, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a.latent), dl, sl, bl, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
+        g_encode(&mv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a.v_cache), dv, sv, bv, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      g_tc_err = "cuTensorMapEncodeTiled failed for the gather maps";
+      return SALS_ERR_CUDA;
+    }
+    e = launch_recon_attn_tc2(map, ml, mv, a, batch, st);
     if (e != cudaSuccess) { g_tc_err = cudaGetErrorString(e); return SALS_ERR_CUDA; }
     return SALS_OK;
   }

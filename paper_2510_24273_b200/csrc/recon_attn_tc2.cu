@@ -35,7 +35,7 @@ constexpr int kVBytes = kRows * kBN * 2;   // 64 KB
 
 __host__ __device__ constexpr int smem_bytes(int G) {
   return 1024 + kStages * (kABytes + kBBytes) + kVBytes + 2 * G * 64 * 8 /*sQ*/ + 2 * 2 * G * kRows * 4 /*sL*/ +
-         2 * G * kRows * 4 /*sP*/ + 1024 /*misc*/;
+         2 * G * kRows * 4 /*sP*/ + 2048 /*misc*/;
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -66,10 +66,24 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map, int col, int r0, int r1, int r2,
+                                            int r3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -113,17 +127,42 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
 struct KArgs {
   TcArgs a;
 };
 
+#ifdef SALS_TC_TRACE
+__device__ unsigned long long g_trace[128];
+#define TSTAMP(slot)                                                                          \
+  do {                                                                                        \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) g_trace[(slot)] = clock64();   \
+  } while (0)
+#else
+#define TSTAMP(slot) do {} while (0)
+#endif
+
 template <int G, int STYLE>
 __global__ void __launch_bounds__(kThreads, 1)
-recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_constant__ KArgs ka) {
+recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_constant__ CUtensorMap tmap_lat,
+                      const __grid_constant__ CUtensorMap tmap_v, const __grid_constant__ KArgs ka) {
   constexpr int NQH = 2 * G;             // query heads of this CTA (2 KV heads)
   const TcArgs& a = ka.a;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align with pointer arithmetic on the __shared__ array so the compiler keeps the shared
+  // address space (an integer round trip would turn every access into a generic load)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = sA + kStages * kABytes;
   uint8_t* sV = sB + kStages * kBBytes;
@@ -131,7 +170,8 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
   float* sL = reinterpret_cast<float*>(sQ + NQH * 64);           // [2 halves][NQH][128] partial logits
   float* sP = sL + 2 * NQH * kRows;                              // [NQH][128] probabilities
   float* sRed = sP + NQH * kRows;                                // [2 kinds][2 halves][4][G]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sRed + 2 * 2 * 4 * G + (G & 1 ? 0 : 0));
+  int* sIdxV = reinterpret_cast<int*>(sRed + 2 * 2 * 4 * G);     // [128] global rows of the V tile
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sIdxV + kRows);
   uint64_t* full = bars;                 // [stages]
   uint64_t* empty = bars + kStages;      // [stages]
   uint64_t* tfull = bars + 2 * kStages;  // [2]
@@ -144,6 +184,7 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
   const int chunk = blockIdx.x, nb = blockIdx.y, b = blockIdx.z;
   const int n0 = nb * kBN;
 
+  if (tid == 0) TSTAMP(80);
   pdl_wait();
   const int cnt = a.count[b];
   const int ntiles_b = (cnt + kRows - 1) / kRows;
@@ -175,12 +216,15 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
                  "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (warp >= 8) {   // rotated, scaled queries: sQ[qh][p] = (q[lo(p)], q[hi(p)])
-    for (int i = tid - 256; i < NQH * 64; i += 256) {
-      const int qh = i >> 6, p = i & 63;
-      const int lo = STYLE == 0 ? p : 2 * p, hi = STYLE == 0 ? p + 64 : 2 * p + 1;
+  if (warp >= 8) {   // rotated, scaled queries: sQ4[qh][p/2] = (q_lo(p), q_lo(p+1), q_hi(p), q_hi(p+1))
+    float4* sQ4 = reinterpret_cast<float4*>(sQ);
+    for (int i = tid - 256; i < NQH * 32; i += 256) {
+      const int qh = i >> 5, p = 2 * (i & 31);
+      const int lo0 = STYLE == 0 ? p : 2 * p, hi0 = STYLE == 0 ? p + 64 : 2 * p + 1;
+      const int lo1 = STYLE == 0 ? p + 1 : 2 * p + 2, hi1 = STYLE == 0 ? p + 65 : 2 * p + 3;
       const float* qr = a.qrope + ((size_t)b * a.n_q + nb * NQH + qh) * kDH;
-      sQ[i] = make_float2(qr[lo] * a.scale_log2, qr[hi] * a.scale_log2);
+      const float sc = a.scale_log2;
+      sQ4[i] = make_float4(qr[lo0] * sc, qr[lo1] * sc, qr[hi0] * sc, qr[hi1] * sc);
     }
   }
   tc_fence_before();
@@ -190,7 +234,7 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
   const int nk = a.r / kBK;
 
   if (warp == 0) {
-    // ================= U (B operand) producer =================
+    // ================= U (B operand) producer: one TMA per K chunk =================
     if (lane == 0) {
       int u = 0;
       for (int it = 0; it < ntile; ++it)
@@ -208,6 +252,7 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
       for (int it = 0; it < ntile; ++it) {
         const int buf = it & 1;
         if (it >= 2) mbar_wait(&tempty[buf], ((it >> 1) - 1) & 1);
+        TSTAMP(0 + it);
         tc_fence_after();
         const uint32_t acc = tmem + buf * kBN;
         for (int kc = 0; kc < nk; ++kc, ++u) {
@@ -222,25 +267,45 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
           mma_commit(&empty[s]);
         }
         mma_commit(&tfull[buf]);
+        TSTAMP(8 + it);
       }
     }
   } else if (warp == 2) {
-    // ================= V rows producer =================
-    if (lane == 0) {
-      const char* vb = reinterpret_cast<const char*>(a.v_cache);
-      for (int it = 0; it < ntile; ++it) {
-        const int tile = t_begin + it;
-        const int nv = min(kRows, cnt - tile * kRows);
-        if (it >= 1) mbar_wait(vempty, (it - 1) & 1);
-        mbar_arrive_expect_tx(vfull, (uint32_t)nv * (kBN * 2));
-        for (int t = 0; t < nv; ++t) {
-          const int row = selb[tile * kRows + t];
-          bulk_load(smem_u32(sV + t * (kBN * 2)), vb + (((size_t)b * a.cap + row) * a.D + n0) * 2, kBN * 2, vfull);
+    // ======== V rows producer: 32 TMA tile::gather4 of 4 x 512-B rows per tile; also
+    // warms L2 with the next tile's V and latent rows ========
+    const char* vb = reinterpret_cast<const char*>(a.v_cache);
+    int* idx = sIdxV;
+    for (int it = 0; it < ntile; ++it) {
+      const int tile = t_begin + it;
+      const int nv = min(kRows, cnt - tile * kRows);
+      if (it >= 1) mbar_wait(vempty, (it - 1) & 1);     // previous tile's P V done with sV (and sIdxV)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int t = lane + 32 * j;
+        idx[t] = t < nv ? b * (int)a.cap + selb[tile * kRows + t] : -1;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_expect_tx(vfull, (uint32_t)kVBytes);
+      __syncwarp();
+      tma_gather4(smem_u32(sV + lane * 4 * (kBN * 2)), &tmap_v, n0, idx[4 * lane], idx[4 * lane + 1],
+                  idx[4 * lane + 2], idx[4 * lane + 3], vfull);
+      if (it + 1 < ntile) {   // next tile's V rows -> L2 via the LSU (keeps the TMA queue for loads)
+        const int ntl = tile + 1;
+        const int nnv = min(kRows, cnt - ntl * kRows);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int t = lane + 32 * j;
+          if (t < nnv) {
+            const char* vr = vb + (((size_t)b * a.cap + selb[ntl * kRows + t]) * a.D + n0) * 2;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) prefetch_l2(vr + c * 128);
+          }
         }
       }
     }
   } else if (warp >= 4 && warp < 8) {
-    // ================= A producers: gathered latent rows =================
+    // ======== A producers: gathered latent rows by 16-byte cp.async into the
+    // SWIZZLE_128B K-major tile (8 lanes per 128-B row chunk, 4 rows per instruction) ========
     const char* latent = reinterpret_cast<const char*>(a.latent);
     const int aw = warp - 4, ch = lane & 7;
     int u = 0;
@@ -282,43 +347,62 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
       const int row = m < nv ? selb[tile * kRows + m] : -1;
       const int pos = (int)a.pos_base + (row >= 0 ? row : 0);
       mbar_wait(&tfull[buf], (it >> 1) & 1);
+      if (ew == 0 && lane == 0) TSTAMP(16 + it);
       tc_fence_after();
-      float part[2][G];
+      float2 part[2][G];         // packed (even pair, odd pair) partial logits per (KV head, query head)
 #pragma unroll
       for (int j = 0; j < 2; ++j)
 #pragma unroll
-        for (int g = 0; g < G; ++g) part[j][g] = 0.f;
+        for (int g = 0; g < G; ++g) part[j][g] = make_float2(0.f, 0.f);
       const uint32_t tacc = tl + buf * kBN;
+      const float4* sQ4 = reinterpret_cast<const float4*>(sQ);
 #pragma unroll 1
       for (int pc = 0; pc < 2; ++pc) {
         const int p0 = 32 * hf + 16 * pc;
+        float xl[2][16], xh[2][16];
+        // issue all four TMEM loads of the chunk, one wait
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          if (STYLE == 0) {
+            tmem_ld16_nowait(tacc + j * kDH + p0, xl[j]);
+            tmem_ld16_nowait(tacc + j * kDH + 64 + p0, xh[j]);
+          } else {
+            tmem_ld16_nowait(tacc + j * kDH + 2 * p0, xl[j]);
+            tmem_ld16_nowait(tacc + j * kDH + 2 * p0 + 16, xh[j]);
+          }
+        }
         float cs[16], sn[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) rope_cs_fast(a.rope.th_hi[p0 + i], a.rope.th_lo[p0 + i], pos, cs[i], sn[i]);
+        tmem_wait_ld();
+        if (STYLE == 1) {   // de-interleave (2i, 2i+1) pairs
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          float xl[16], xh[16];
-          if (STYLE == 0) {
-            tmem_ld16(tacc + j * kDH + p0, xl);
-            tmem_ld16(tacc + j * kDH + 64 + p0, xh);
-          } else {
+          for (int j = 0; j < 2; ++j) {
             float t0[16], t1[16];
-            tmem_ld16(tacc + j * kDH + 2 * p0, t0);
-            tmem_ld16(tacc + j * kDH + 2 * p0 + 16, t1);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) { t0[i] = xl[j][i]; t1[i] = xh[j][i]; }
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-              xl[i] = t0[2 * i]; xh[i] = t0[2 * i + 1];
-              xl[8 + i] = t1[2 * i]; xh[8 + i] = t1[2 * i + 1];
+              xl[j][i] = t0[2 * i]; xh[j][i] = t0[2 * i + 1];
+              xl[j][8 + i] = t1[2 * i]; xh[j][8 + i] = t1[2 * i + 1];
             }
           }
+        }
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float rl = xl[i] * cs[i] - xh[i] * sn[i];
-            const float rh = xl[i] * sn[i] + xh[i] * cs[i];
+        for (int i = 0; i < 16; i += 2) {
+          const float2 c2 = make_float2(cs[i], cs[i + 1]);
+          const float2 s2 = make_float2(sn[i], sn[i + 1]);
+          const float2 ns2 = make_float2(-sn[i], -sn[i + 1]);
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const float2 xl2 = make_float2(xl[j][i], xl[j][i + 1]);
+            const float2 xh2 = make_float2(xh[j][i], xh[j][i + 1]);
+            const float2 rl = __ffma2_rn(xl2, c2, __fmul2_rn(xh2, ns2));   // x_lo c - x_hi s
+            const float2 rh = __ffma2_rn(xl2, s2, __fmul2_rn(xh2, c2));    // x_lo s + x_hi c
 #pragma unroll
             for (int g = 0; g < G; ++g) {
-              const float2 q = sQ[(j * G + g) * 64 + p0 + i];
-              part[j][g] = fmaf(q.x, rl, fmaf(q.y, rh, part[j][g]));
+              const float4 q = sQ4[(j * G + g) * 32 + ((p0 + i) >> 1)];
+              part[j][g] = __ffma2_rn(make_float2(q.x, q.y), rl, __ffma2_rn(make_float2(q.z, q.w), rh, part[j][g]));
             }
           }
         }
@@ -329,8 +413,9 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
 #pragma unroll
       for (int j = 0; j < 2; ++j)
 #pragma unroll
-        for (int g = 0; g < G; ++g) sL[(hf * NQH + j * G + g) * kRows + m] = part[j][g];
+        for (int g = 0; g < G; ++g) sL[(hf * NQH + j * G + g) * kRows + m] = part[j][g].x + part[j][g].y;
       bar_epi();
+      if (ew == 0 && lane == 0) TSTAMP(24 + it);
       // ---- half hf owns KV head hf: full logits, tile softmax, online rescale
       float lg[G], mnew[G], alpha[G];
 #pragma unroll
@@ -366,16 +451,36 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
         o[g] *= alpha[g];
       }
       mbar_wait(vfull, it & 1);
+      if (ew == 0 && lane == 0) TSTAMP(32 + it);
       // ---- P V over the staged rows: dim n of KV head hf
       const unsigned short* vcol = reinterpret_cast<const unsigned short*>(sV) + hf * kDH + n;
       const float* pp = sP + hf * G * kRows;
-#pragma unroll 4
-      for (int t = 0; t < nv; ++t) {
+      float2 oa[G], ob[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) oa[g] = ob[g] = make_float2(0.f, 0.f);
+      int t = 0;
+#pragma unroll 2
+      for (; t + 4 <= nv; t += 4) {
+        const float2 va = make_float2(__uint_as_float((uint32_t)vcol[t * kBN] << 16),
+                                      __uint_as_float((uint32_t)vcol[(t + 1) * kBN] << 16));
+        const float2 vb = make_float2(__uint_as_float((uint32_t)vcol[(t + 2) * kBN] << 16),
+                                      __uint_as_float((uint32_t)vcol[(t + 3) * kBN] << 16));
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const float4 p4 = *reinterpret_cast<const float4*>(pp + g * kRows + t);
+          oa[g] = __ffma2_rn(make_float2(p4.x, p4.y), va, oa[g]);
+          ob[g] = __ffma2_rn(make_float2(p4.z, p4.w), vb, ob[g]);
+        }
+      }
+      for (; t < nv; ++t) {
         const float v = __uint_as_float((uint32_t)vcol[t * kBN] << 16);
 #pragma unroll
-        for (int g = 0; g < G; ++g) o[g] = fmaf(pp[g * kRows + t], v, o[g]);
+        for (int g = 0; g < G; ++g) oa[g].x = fmaf(pp[g * kRows + t], v, oa[g].x);
       }
+#pragma unroll
+      for (int g = 0; g < G; ++g) o[g] += (oa[g].x + oa[g].y) + (ob[g].x + ob[g].y);
       bar_epi();                                       // sV / sP / sL / sRed free
+      if (ew == 0 && lane == 0) TSTAMP(40 + it);
       if (ew == 0 && lane == 0) mbar_arrive(vempty);
     }
     // ---- write y (single chunk) or the chunk's partial
@@ -394,6 +499,7 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
   }
   tc_fence_before();
   __syncthreads();
+  if (tid == 0) TSTAMP(81);
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();
@@ -403,7 +509,8 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
 }
 
 template <int G, int STYLE>
-cudaError_t launch_t(const CUtensorMap& map, const TcArgs& a, int batch, cudaStream_t st) {
+cudaError_t launch_t(const CUtensorMap& map, const CUtensorMap& map_lat, const CUtensorMap& map_v, const TcArgs& a,
+                     int batch, cudaStream_t st) {
   auto kern = recon_attn_tc2_kernel<G, STYLE>;
   static bool attr = false;
   if (!attr) {
@@ -422,21 +529,31 @@ cudaError_t launch_t(const CUtensorMap& map, const TcArgs& a, int batch, cudaStr
   cfg.attrs = at;
   cfg.numAttrs = 1;
   KArgs ka{a};
-  return cudaLaunchKernelEx(&cfg, kern, map, ka);
+  return cudaLaunchKernelEx(&cfg, kern, map, map_lat, map_v, ka);
 }
 
 }  // namespace tc2
+
+extern "C" int sals_debug_tc_trace(unsigned long long* host_out) {
+#ifdef SALS_TC_TRACE
+  return (int)cudaMemcpyFromSymbol(host_out, tc2::g_trace, sizeof(tc2::g_trace));
+#else
+  (void)host_out;
+  return -1;
+#endif
+}
 
 bool tc2_supported(int head_dim, int D, int rank, int G) {
   return head_dim == 128 && D % tc2::kBN == 0 && rank % tc2::kBK == 0 && (G == 1 || G == 2 || G == 4);
 }
 
-cudaError_t launch_recon_attn_tc2(const CUtensorMap& map, const TcArgs& a, int batch, cudaStream_t st) {
+cudaError_t launch_recon_attn_tc2(const CUtensorMap& map, const CUtensorMap& ml, const CUtensorMap& mv,
+                                  const TcArgs& a, int batch, cudaStream_t st) {
   const int style = a.rope.style;
   switch (a.G) {
-    case 1: return style ? tc2::launch_t<1, 1>(map, a, batch, st) : tc2::launch_t<1, 0>(map, a, batch, st);
-    case 2: return style ? tc2::launch_t<2, 1>(map, a, batch, st) : tc2::launch_t<2, 0>(map, a, batch, st);
-    case 4: return style ? tc2::launch_t<4, 1>(map, a, batch, st) : tc2::launch_t<4, 0>(map, a, batch, st);
+    case 1: return style ? tc2::launch_t<1, 1>(map, ml, mv, a, batch, st) : tc2::launch_t<1, 0>(map, ml, mv, a, batch, st);
+    case 2: return style ? tc2::launch_t<2, 1>(map, ml, mv, a, batch, st) : tc2::launch_t<2, 0>(map, ml, mv, a, batch, st);
+    case 4: return style ? tc2::launch_t<4, 1>(map, ml, mv, a, batch, st) : tc2::launch_t<4, 0>(map, ml, mv, a, batch, st);
   }
   return cudaErrorInvalidValue;
 }

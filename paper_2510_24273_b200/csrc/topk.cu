@@ -23,9 +23,11 @@
 namespace sals {
 
 constexpr int kTopkWarps = kTopkThreads / 32;
+constexpr int kMaxCluster = 16;
 
-// Inclusive scan of one value per thread across the 512-thread block.
-__device__ __forceinline__ int block_incl_scan(int v, int* warp_tot) {
+// Inclusive scan of one value per thread across the 512-thread block; *total
+// receives the block-wide sum (same value in every thread).
+__device__ __forceinline__ int block_incl_scan(int v, int* warp_tot, int* total = nullptr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -46,6 +48,7 @@ __device__ __forceinline__ int block_incl_scan(int v, int* warp_tot) {
   __syncthreads();
   const int add = (warp > 0) ? warp_tot[warp - 1] : 0;
   const int r = v + add;
+  if (total) *total = warp_tot[kTopkWarps - 1];
   __syncthreads();
   return r;
 }
@@ -53,9 +56,12 @@ __device__ __forceinline__ int block_incl_scan(int v, int* warp_tot) {
 __global__ void __launch_bounds__(kTopkThreads)
 topk_cluster_kernel(TopkArgs a) {
   extern __shared__ __align__(16) uint8_t tk_smem[];
-  __shared__ uint32_t whist[kTopkWarps][256];
-  __shared__ uint32_t chist[2][256];
-  __shared__ int xch[4];           // cluster-visible: [0] ranked count, [1] definite count, [2] tie count
+  // Cluster exchange is push-based: every CTA stores its values into a slot of
+  // EVERY peer's shared memory (fire-and-forget st.shared::cluster), so after
+  // the cluster barrier all reads are local.
+  __shared__ uint32_t inc_hist[2][kMaxCluster][256];   // [pass parity][source rank][digit]
+  __shared__ uint32_t s_tot[256];
+  __shared__ int inc_cnt[kMaxCluster][4];              // [source rank]: ranked, definite, ties
   __shared__ int warp_tot[32];
   __shared__ int s_digit, s_need, s_nranked;
 
@@ -67,8 +73,11 @@ topk_cluster_kernel(TopkArgs a) {
   uint32_t* keys = reinterpret_cast<uint32_t*>(tk_smem);
   uint8_t* cls = tk_smem + (size_t)slice * 4;   // 0 none, 1 forced, 2 ranked
   // global indices are only stored when they come from a candidate list
-  int* gidx = a.cand_idx ? reinterpret_cast<int*>(tk_smem + (size_t)slice * 5 + ((16 - (slice * 5) % 16) % 16))
-                         : nullptr;
+  const size_t gidx_off = ((size_t)slice * 5 + 15) / 16 * 16;
+  int* gidx = a.cand_idx ? reinterpret_cast<int*>(tk_smem + gidx_off) : nullptr;
+  // per-warp digit histograms after the key / class / index arrays
+  uint32_t (*whist)[256] = reinterpret_cast<uint32_t (*)[256]>(
+      tk_smem + gidx_off + (a.cand_idx ? (size_t)slice * 4 : 0));
 
   pdl_wait();
   const int s = a.seq_len[b];
@@ -97,13 +106,15 @@ topk_cluster_kernel(TopkArgs a) {
     my_ranked += (c == 2);
   }
   {
-    int tot = block_incl_scan(my_ranked, warp_tot);
-    if (tid == kTopkThreads - 1) xch[0] = tot;
+    int tot;
+    block_incl_scan(my_ranked, warp_tot, &tot);
+    if (tid >= kTopkThreads - 32 && tid - (kTopkThreads - 32) < CS)
+      st_dsmem_u32(mapa_shared(smem_u32(&inc_cnt[rank][0]), tid - (kTopkThreads - 32)), (uint32_t)tot);
   }
   cluster_sync_all();
   if (tid == 0) {
     int nr = 0;
-    for (int c = 0; c < CS; ++c) nr += (int)ld_dsmem_u32(mapa_shared(smem_u32(&xch[0]), c));
+    for (int c = 0; c < CS; ++c) nr += inc_cnt[c][0];
     int nd = (a.mode == 0) ? (all_mode0 ? 0 : a.k - x - z) : (a.k - x - z);
     s_nranked = nr;
     s_need = max(0, min(nd, nr));
@@ -140,25 +151,25 @@ topk_cluster_kernel(TopkArgs a) {
         if (ok && lane == __ffs(peers) - 1) atomicAdd(&whist[warp][dg], (uint32_t)__popc(peers));
       }
       __syncthreads();
-      uint32_t* ch = chist[pass & 1];
       if (tid < 256) {
         uint32_t t = 0;
 #pragma unroll
         for (int w = 0; w < kTopkWarps; ++w) { t += whist[w][tid]; whist[w][tid] = 0; }
-        ch[tid] = t;
+        const uint32_t addr = smem_u32(&inc_hist[pass & 1][rank][tid]);
+        for (int c = 0; c < CS; ++c) st_dsmem_u32(mapa_shared(addr, c), t);
       }
       cluster_sync_all();
+      if (tid < 256) {
+        uint32_t t = 0;
+        for (int c = 0; c < CS; ++c) t += inc_hist[pass & 1][c][tid];
+        s_tot[tid] = t;
+      }
+      __syncthreads();
       if (warp == 0) {
-        // lane l owns digits 255 - 8l - j, j = 0..7 (descending); counts summed over the cluster
+        // lane l owns digits 255 - 8l - j, j = 0..7 (descending)
         int c8[8], tot = 0;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint32_t addr = smem_u32(&ch[255 - 8 * lane - j]);
-          int v = 0;
-          for (int c = 0; c < CS; ++c) v += (int)ld_dsmem_u32(mapa_shared(addr, c));
-          c8[j] = v;
-          tot += v;
-        }
+        for (int j = 0; j < 8; ++j) { c8[j] = (int)s_tot[255 - 8 * lane - j]; tot += c8[j]; }
         int incl = tot;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
@@ -191,18 +202,23 @@ topk_cluster_kernel(TopkArgs a) {
     if (c == 1 || (c == 2 && keys[i] > T)) ++n_def;
     else if (c == 2 && keys[i] == T) ++n_eq;
   }
-  const int def_incl = block_incl_scan(n_def, warp_tot);
-  const int eq_incl = block_incl_scan(n_eq, warp_tot);
-  if (tid == kTopkThreads - 1) { xch[1] = def_incl; xch[2] = eq_incl; }
+  int def_cta, eq_cta;
+  const int def_incl = block_incl_scan(n_def, warp_tot, &def_cta);
+  const int eq_incl = block_incl_scan(n_eq, warp_tot, &eq_cta);
+  if (tid >= kTopkThreads - 32 && tid - (kTopkThreads - 32) < CS) {
+    const int c = tid - (kTopkThreads - 32);
+    st_dsmem_u32(mapa_shared(smem_u32(&inc_cnt[rank][1]), c), (uint32_t)def_cta);
+    st_dsmem_u32(mapa_shared(smem_u32(&inc_cnt[rank][2]), c), (uint32_t)eq_cta);
+  }
   cluster_sync_all();
   int def_before = 0, eq_before = 0, def_total = 0, eq_total = 0;
   for (int c = 0; c < CS; ++c) {
-    const int dc = (int)ld_dsmem_u32(mapa_shared(smem_u32(&xch[1]), c));
-    const int ec = (int)ld_dsmem_u32(mapa_shared(smem_u32(&xch[2]), c));
+    const int dc = inc_cnt[c][1];
+    const int ec = inc_cnt[c][2];
     if (c < rank) { def_before += dc; eq_before += ec; }
     def_total += dc; eq_total += ec;
   }
-  const int eq_local = xch[2];
+  const int eq_local = inc_cnt[rank][2];
   const int take_local = max(0, min(need_eq - eq_before, eq_local));
   const int out_base = def_before + min(need_eq, eq_before);
   const int count = def_total + min(need_eq, eq_total);
