@@ -177,6 +177,13 @@ int flash_tpw_unr(const sals_config* c) {
   return (32 / lpt) * 2;
 }
 
+// Rows of U per CTA of the projection cluster: a multiple of 8 (16-byte vectors).
+void plan_proj(Plan& p) {
+  const int cs = std::min(16, std::max(1, ceil_div(p.D, 64)));
+  p.proj_rows = (int)align_up(ceil_div(p.D, cs), 8);
+  p.proj_cs = ceil_div(p.D, p.proj_rows);
+}
+
 sals_status make_plan(const sals_config* c, int batch, int max_s, Plan& p, bool for_size) {
   p.D = c->num_kv_heads * c->head_dim;
   p.G = c->num_q_heads / c->num_kv_heads;
@@ -200,8 +207,7 @@ sals_status make_plan(const sals_config* c, int batch, int max_s, Plan& p, bool 
   }
   sals_status st = plan_topk(max_s, false, p);
   if (st != SALS_OK) return st;
-  p.proj_cs = std::min(16, std::max(1, ceil_div(p.D, 64)));
-  p.proj_rows = ceil_div(p.D, p.proj_cs);
+  plan_proj(p);
   const size_t es = esize(c);
   p.score_stride = (int64_t)align_up(max_s, 4);
   size_t off = 0;
@@ -452,8 +458,7 @@ sals_status sals_append_latent(const sals_config* cfg, const void* U, const void
   if (batch < 1 || batch > 65535 || cap < 1) return fail(SALS_ERR_INVALID_ARGUMENT, "bad batch / cap");
   Plan p{};
   p.D = cfg->num_kv_heads * cfg->head_dim;
-  p.proj_cs = std::min(16, std::max(1, ceil_div(p.D, 64)));
-  p.proj_rows = ceil_div(p.D, p.proj_cs);
+  plan_proj(p);
   ProjectArgs a{};
   a.U = U; a.x = k_new; a.x_stride = p.D; a.D = p.D; a.r = cfg->rank; a.ncols = cfg->rank; a.B = batch;
   a.head_dim = cfg->head_dim; a.group = 1; a.n_q = cfg->num_q_heads; a.latent = latent_cache; a.cap = cap;

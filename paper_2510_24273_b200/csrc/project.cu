@@ -100,20 +100,33 @@ project_kernel(ProjectArgs a) {
 
   for (int b0 = 0; b0 < a.B; b0 += kProjBT) {
     const int nb = min(kProjBT, a.B - b0);
-    // stage x (pooled over the query heads of each KV group for qproj)
-    for (int i = tid; i < kProjBT * rows_per; i += kProjThreads) {
-      const int bb = i / rows_per, c = row0 + i % rows_per;
-      float v = 0.f;
-      if (bb < nb && c < row1) {
-        const T* xb = x + (size_t)(b0 + bb) * a.x_stride;
-        if (POOL) {
-          const int g = c / a.head_dim, j = c % a.head_dim;
-          for (int hh = 0; hh < a.group; ++hh) v += Elem<T>::to_f(xb[(g * a.group + hh) * a.head_dim + j]);
-        } else {
-          v = Elem<T>::to_f(xb[c]);
+    // stage x (pooled over the query heads of each KV group for qproj): one
+    // 16-byte vector per thread per head, all loads issued before the sums
+    {
+      const int nvec_row = (row1 - row0) / EPC;          // rows_per is a multiple of EPC
+      for (int i = tid; i < kProjBT * nvec_row; i += kProjThreads) {
+        const int bb = i / nvec_row, cv = i - bb * nvec_row;
+        const int c = row0 + cv * EPC;
+        float v[EPC];
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) v[e] = 0.f;
+        if (bb < nb) {
+          const T* xb = x + (size_t)(b0 + bb) * a.x_stride;
+          if (POOL) {
+            const int g = c / a.head_dim, j = c - g * a.head_dim;   // EPC <= head_dim: one head per vector
+            for (int hh = 0; hh < a.group; ++hh) {
+              float f[EPC];
+              Elem<T>::unpack(ld_v4(xb + (g * a.group + hh) * a.head_dim + j), f);
+#pragma unroll
+              for (int e = 0; e < EPC; ++e) v[e] += f[e];
+            }
+          } else {
+            Elem<T>::unpack(ld_v4(xb + c), v);
+          }
         }
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) xs[bb][cv * EPC + e] = v[e];
       }
-      xs[bb][i % rows_per] = v;
     }
     __syncthreads();
 

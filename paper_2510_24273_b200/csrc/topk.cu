@@ -87,23 +87,40 @@ topk_cluster_kernel(TopkArgs a) {
   const int x = a.sink, z = a.recent;
   const bool all_mode0 = (a.mode == 0) && (s <= a.k);
 
-  // ---- load slice -> keys / classes -------------------------------------
+  // ---- load slice -> keys / classes (4 independent loads in flight per thread) ----
   int my_ranked = 0;
-  for (int i = tid; i < nloc; i += kTopkThreads) {
-    const int e = e0 + i;
-    const size_t off = a.seg_len > 0 ? (size_t)(e / a.seg_len) * a.seg_stride + (size_t)b * a.seg_len + e % a.seg_len
-                                     : (size_t)b * a.score_stride + e;
-    const int idx = a.cand_idx ? a.cand_idx[off] : (int)(a.idx_base + e);
-    uint8_t c = 0;
-    if (idx >= 0 && idx < s) {
-      const bool in_rank = (idx >= x) && (idx < s - z);
-      if (a.mode == 0) c = (all_mode0 || !in_rank) ? 1 : 2;
-      else c = in_rank ? 2 : 0;
+  for (int i0 = tid; i0 < nloc; i0 += 4 * kTopkThreads) {
+    float sc[4];
+    int ix[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * kTopkThreads;
+      sc[u] = 0.f;
+      ix[u] = -1;
+      if (i < nloc) {
+        const int e = e0 + i;
+        const size_t off = a.seg_len > 0 ? (size_t)(e / a.seg_len) * a.seg_stride + (size_t)b * a.seg_len + e % a.seg_len
+                                         : (size_t)b * a.score_stride + e;
+        ix[u] = a.cand_idx ? a.cand_idx[off] : (int)(a.idx_base + e);
+        sc[u] = a.scores[off];
+      }
     }
-    keys[i] = (c == 2) ? float_key(a.scores[off]) : 0u;
-    cls[i] = c;
-    if (gidx) gidx[i] = idx;
-    my_ranked += (c == 2);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * kTopkThreads;
+      if (i >= nloc) continue;
+      const int idx = ix[u];
+      uint8_t c = 0;
+      if (idx >= 0 && idx < s) {
+        const bool in_rank = (idx >= x) && (idx < s - z);
+        if (a.mode == 0) c = (all_mode0 || !in_rank) ? 1 : 2;
+        else c = in_rank ? 2 : 0;
+      }
+      keys[i] = (c == 2) ? float_key(sc[u]) : 0u;
+      cls[i] = c;
+      if (gidx) gidx[i] = idx;
+      my_ranked += (c == 2);
+    }
   }
   {
     int tot;
@@ -136,19 +153,13 @@ topk_cluster_kernel(TopkArgs a) {
     __syncthreads();
     for (int pass = 0; pass < 4; ++pass) {
       const int shift = 24 - 8 * pass;
-      // per-warp histogram of the digit, warp-aggregated (few distinct digits per warp)
-      for (int base = warp * 32; base < nloc; base += kTopkThreads) {
-        const int i = base + lane;
-        bool ok = false;
-        uint32_t dg = 0;
-        if (i < nloc && cls[i] == 2) {
-          const uint32_t key = keys[i];
-          ok = (pass == 0) || (((key ^ prefix) >> (shift + 8)) == 0);
-          dg = (key >> shift) & 255u;
-        }
-        const uint32_t tag = ok ? dg : (256u + lane);
-        const uint32_t peers = __match_any_sync(0xffffffffu, tag);
-        if (ok && lane == __ffs(peers) - 1) atomicAdd(&whist[warp][dg], (uint32_t)__popc(peers));
+      // per-warp histogram of the digit (shared-memory atomics; a fully conflicting
+      // warp costs ~32 cycles, cheaper than aggregating with match.any)
+      for (int i = tid; i < nloc; i += kTopkThreads) {
+        if (cls[i] != 2) continue;
+        const uint32_t key = keys[i];
+        if (pass > 0 && ((key ^ prefix) >> (shift + 8)) != 0) continue;
+        atomicAdd(&whist[warp][(key >> shift) & 255u], 1u);
       }
       __syncthreads();
       if (tid < 256) {

@@ -1,7 +1,7 @@
 """Top source lines by warp-stall samples and stall reasons from an ncu report."""
 import csv, subprocess, sys
 rep = sys.argv[1]
-KF = (["-k", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else [])
+KF = (["-k", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []) + (["-s", sys.argv[4], "-c", "1"] if len(sys.argv) > 4 else [])
 raw = subprocess.run(["ncu", "-i", rep, *KF, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(raw.splitlines()))
 hdr, vals = rows[0], rows[2]
