@@ -136,10 +136,11 @@ struct Plan {
   int nsplit, chunk;       // flash split (SIMT) / 128-row tiles (tc v1) / chunks + tiles per CTA (tc v2)
   bool tc2;
   int tk_cs, tk_slice;     // top-k cluster size / slice
+  int tk_nt, tk_cap;       // threads per CTA, candidate capacity (histogram-assisted kernel)
   size_t tk_smem;
   int proj_cs, proj_rows;
   // workspace offsets
-  size_t off_qtil, off_qrope, off_scores, off_sel, off_count, off_kr, off_part, total;
+  size_t off_qtil, off_qrope, off_scores, off_sel, off_count, off_kr, off_part, off_hist, total;
   int64_t score_stride;
 };
 
@@ -149,6 +150,9 @@ bool tc_eligible(const sals_config* c, int batch, int kmax) {
          c->num_q_heads / c->num_kv_heads);
 }
 
+// Top-k cluster plan.  cand == true: the generic kernel over all-gathered
+// candidates (K9); else the histogram-assisted kernel (K4 / K8).
+constexpr size_t kTopkDynSmem = 190 * 1024;
 sals_status plan_topk(int n_entries, bool cand, Plan& p) {
   int cs = 1;
   while (cs < 16 && ceil_div(n_entries, cs) > 2048) cs <<= 1;
@@ -158,7 +162,15 @@ sals_status plan_topk(int n_entries, bool cand, Plan& p) {
   if (slice > cap) return fail(SALS_ERR_UNSUPPORTED, "top-k over %d entries exceeds the cluster limit", n_entries);
   p.tk_cs = cs;
   p.tk_slice = slice;
-  p.tk_smem = ((size_t)slice * 5 + 15) / 16 * 16 + (cand ? (size_t)slice * 4 : 0) + (size_t)(kTopkThreads / 32) * 256 * 4;
+  if (cand) {
+    p.tk_nt = kTopkThreads;
+    p.tk_cap = 0;
+    p.tk_smem = ((size_t)slice * 9 + 15) / 16 * 16 + (size_t)(kTopkThreads / 32) * 256 * 4;
+  } else {
+    p.tk_nt = slice >= 4096 ? 1024 : 512;
+    p.tk_cap = (int)std::min<size_t>(kCandCap, (kTopkDynSmem - (size_t)slice * 8) / 4);
+    p.tk_smem = (size_t)slice * 8 + (size_t)p.tk_cap * 4;
+  }
   return SALS_OK;
 }
 
@@ -219,6 +231,7 @@ sals_status make_plan(const sals_config* c, int batch, int max_s, Plan& p, bool 
   p.off_count = take((size_t)batch * 4);
   p.off_kr = take(p.tc ? 0 : (size_t)batch * c->top_k * p.D * es);
   p.off_part = take((size_t)batch * c->num_q_heads * p.nsplit * (c->head_dim + 2) * 4);
+  p.off_hist = take((size_t)batch * kH0Bins * 4);
   p.total = off;
   return SALS_OK;
 }
@@ -272,14 +285,29 @@ sals_status launch_score(const sals_config* c, ScoreArgs a, int batch, int max_l
   return SALS_OK;
 }
 
-sals_status launch_topk(const TopkArgs& a, int batch, int cs, size_t smem, cudaStream_t st) {
+sals_status launch_topk(TopkArgs a, int batch, const Plan& p, cudaStream_t st) {
   static bool attr_done = false;
   if (!attr_done) {
-    SALS_CUDA_TRY(cudaFuncSetAttribute(topk_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 180 * 1024));
+    auto* k512 = topk_hist_kernel<512>;
+    auto* k1024 = topk_hist_kernel<1024>;
+    SALS_CUDA_TRY(cudaFuncSetAttribute(topk_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTopkDynSmem));
     SALS_CUDA_TRY(cudaFuncSetAttribute(topk_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    SALS_CUDA_TRY(cudaFuncSetAttribute(k512, cudaFuncAttributeMaxDynamicSharedMemorySize, kTopkDynSmem));
+    SALS_CUDA_TRY(cudaFuncSetAttribute(k512, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    SALS_CUDA_TRY(cudaFuncSetAttribute(k1024, cudaFuncAttributeMaxDynamicSharedMemorySize, kTopkDynSmem));
+    SALS_CUDA_TRY(cudaFuncSetAttribute(k1024, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr_done = true;
   }
-  SALS_CUDA_TRY(launch(topk_cluster_kernel, dim3(batch * cs), dim3(kTopkThreads), smem, st, cs, a));  // cluster attr even for cs == 1
+  // cluster attribute even for cs == 1 (the kernels use cluster barriers / DSMEM)
+  if (a.hist0 == nullptr) {
+    SALS_CUDA_TRY(launch(topk_cluster_kernel, dim3(batch * p.tk_cs), dim3(kTopkThreads), p.tk_smem, st, p.tk_cs, a));
+  } else {
+    a.cand_cap = p.tk_cap;
+    if (p.tk_nt == 1024)
+      SALS_CUDA_TRY(launch(topk_hist_kernel<1024>, dim3(batch * p.tk_cs), dim3(1024), p.tk_smem, st, p.tk_cs, a));
+    else
+      SALS_CUDA_TRY(launch(topk_hist_kernel<512>, dim3(batch * p.tk_cs), dim3(512), p.tk_smem, st, p.tk_cs, a));
+  }
   return SALS_OK;
 }
 
@@ -395,6 +423,8 @@ sals_status decode_impl(const sals_config* c, const void* U, const void* q, cons
   pa.U = U; pa.x = q; pa.x_stride = c->num_q_heads * c->head_dim; pa.D = p.D; pa.r = c->rank;
   pa.ncols = c->score_rank; pa.B = batch; pa.head_dim = c->head_dim; pa.group = p.G;
   pa.n_q = c->num_q_heads; pa.out_f32 = qtil; pa.qrope = qrope; pa.seq_len = seq_len; pa.rope = make_rope(c);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(ws + p.off_hist);
+  pa.hist0_zero = hist; pa.hist0_words = batch * kH0Bins;
   mark_begin(st);
   sals_status s = launch_project<T>(c, p, true, pa, c->score_rank, st);
   if (s != SALS_OK) return s;
@@ -403,6 +433,7 @@ sals_status decode_impl(const sals_config* c, const void* U, const void* q, cons
   ScoreArgs sa{};
   sa.latent = latent; sa.cap = cap; sa.r = c->rank; sa.rstar = c->score_rank; sa.qtil = qtil;
   sa.len = seq_len; sa.scores = scores; sa.stride = sstride;
+  sa.hist0 = hist; sa.seq_len = seq_len; sa.idx_base = 0; sa.sink = c->sink; sa.recent = c->recent;
   s = launch_score<T>(c, sa, batch, max_s, st);
   if (s != SALS_OK) return s;
   mark(kStScore, st);
@@ -412,7 +443,8 @@ sals_status decode_impl(const sals_config* c, const void* U, const void* q, cons
   ta.k = c->top_k; ta.sink = c->sink; ta.recent = c->recent; ta.mode = 0; ta.slice = p.tk_slice;
   ta.sel_out = sel; ta.sel_stride = c->top_k; ta.sel_count = count; ta.pad_to = c->top_k;
   ta.sel_out2 = sel_out;
-  s = launch_topk(ta, batch, p.tk_cs, p.tk_smem, st);
+  ta.hist0 = hist;
+  s = launch_topk(ta, batch, p, st);
   if (s != SALS_OK) return s;
   mark(kStTopk, st);
 
@@ -627,9 +659,12 @@ sals_status sals_shard_candidates(const sals_config* cfg, const void* U, const v
   pa.ncols = cfg->score_rank; pa.B = batch; pa.head_dim = cfg->head_dim; pa.group = p.G; pa.n_q = cfg->num_q_heads;
   pa.out_f32 = qtil; pa.qrope = reinterpret_cast<float*>(ws + p.off_qrope); pa.seq_len = d_seq_len;
   pa.rope = make_rope(cfg);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(ws + p.off_hist);
+  pa.hist0_zero = hist; pa.hist0_words = batch * kH0Bins;
   ScoreArgs sa{};
   sa.latent = latent_shard; sa.cap = cap_local; sa.r = cfg->rank; sa.rstar = cfg->score_rank; sa.qtil = qtil;
   sa.len = d_local_len; sa.scores = scores; sa.stride = p.score_stride;
+  sa.hist0 = hist; sa.seq_len = d_seq_len; sa.idx_base = shard_start; sa.sink = cfg->sink; sa.recent = cfg->recent;
   if (cfg->dtype == SALS_BF16) {
     s = launch_project<__nv_bfloat16>(cfg, p, true, pa, cfg->score_rank, st);
     if (s == SALS_OK) s = launch_score<__nv_bfloat16>(cfg, sa, batch, max_local_len, st);
@@ -643,7 +678,8 @@ sals_status sals_shard_candidates(const sals_config* cfg, const void* U, const v
   ta.idx_base = shard_start; ta.k = cfg->top_k; ta.sink = cfg->sink; ta.recent = cfg->recent; ta.mode = 1;
   ta.slice = p.tk_slice; ta.sel_out = cand_idx; ta.sel_stride = cfg->top_k; ta.sel_score = cand_score;
   ta.pad_to = cfg->top_k;
-  return launch_topk(ta, batch, p.tk_cs, p.tk_smem, st);
+  ta.hist0 = hist;
+  return launch_topk(ta, batch, p, st);
 }
 
 sals_status sals_shard_attend(const sals_config* cfg, const void* U, const void* q, const void* latent_shard,
@@ -678,7 +714,7 @@ sals_status sals_shard_attend(const sals_config* cfg, const void* U, const void*
   ta.seg_len = cfg->top_k; ta.seg_stride = (int64_t)batch * cfg->top_k; ta.seq_len = d_seq_len;
   ta.k = cfg->top_k; ta.sink = cfg->sink; ta.recent = cfg->recent; ta.mode = 1; ta.slice = pk.tk_slice;
   ta.sel_out = gsel; ta.sel_stride = cfg->top_k; ta.sel_count = gcount; ta.pad_to = cfg->top_k;
-  s = launch_topk(ta, batch, pk.tk_cs, pk.tk_smem, st);
+  s = launch_topk(ta, batch, pk, st);
   if (s != SALS_OK) return s;
   OwnedArgs oa{};
   oa.gsel = gsel; oa.gcount = gcount; oa.g_stride = cfg->top_k; oa.seq_len = d_seq_len; oa.local_len = d_local_len;

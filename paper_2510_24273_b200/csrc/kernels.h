@@ -13,7 +13,11 @@ namespace sals {
 // Block sizes shared by kernels and launcher.
 constexpr int kProjThreads = 256;
 constexpr int kScoreThreads = 256;
-constexpr int kTopkThreads = 512;
+constexpr int kTopkThreads = 1024;
+// First radix digit of the top-k, built by the score kernel: the top 11 bits of
+// the order-preserving float key of every ranked score.
+constexpr int kH0Bits = 11, kH0Bins = 1 << kH0Bits, kH0Shift = 32 - kH0Bits;
+constexpr int kCandCap = 12288;   // threshold-bin candidate keys held by every top-k CTA (48 KB)
 
 struct ProjectArgs {
   const void* U;        // [D, r]
@@ -30,6 +34,7 @@ struct ProjectArgs {
   // append outputs
   void* latent; int64_t cap; const int* pos;
   const void* v_new; void* v_cache;
+  uint32_t* hist0_zero; int hist0_words;   // qproj: zero the score histogram (rope-role CTAs)
 };
 
 struct ScoreArgs {
@@ -40,6 +45,10 @@ struct ScoreArgs {
   float* scores;        // [B, stride]
   int64_t stride;
   int tokens_per_cta;
+  uint32_t* hist0;      // nullable [B, kH0Bins]: top-digit histogram of the ranked scores (zeroed upstream)
+  const int* seq_len;   // [B] global s_b (ranked range [sink, s_b - recent))
+  int64_t idx_base;     // global index of local token 0
+  int sink, recent;
 };
 
 struct TopkArgs {
@@ -59,6 +68,8 @@ struct TopkArgs {
   int* sel_out2;          // nullable second copy of sel_out (user buffer), stride sel_stride
   int seg_len;            // >0: entries are [world][B][seg_len] (all-gathered candidates)
   int64_t seg_stride;     //     = B * seg_len
+  const uint32_t* hist0;  // nullable [B, kH0Bins] from the score kernel: histogram-assisted path
+  int cand_cap;           // histogram-assisted path: capacity of the cluster-wide candidate array
 };
 
 struct ReconArgs {        // SIMT reconstruct + RoPE (path S)
@@ -108,6 +119,7 @@ struct OwnedArgs {        // sharded: owned selection list = owned sinks | owned
 template <typename T, bool POOL> __global__ void project_kernel(ProjectArgs a);
 template <typename T, int LG, int CPL> __global__ void latent_score_kernel(ScoreArgs a);
 __global__ void topk_cluster_kernel(TopkArgs a);
+template <int NT> __global__ void topk_hist_kernel(TopkArgs a);
 template <typename T> __global__ void recon_rope_simt_kernel(ReconArgs a);
 template <typename T, int DH, int G, bool DENSE> __global__ void flash_decode_kernel(FlashArgs a);
 template <typename T> __global__ void merge_kernel(MergeArgs a);

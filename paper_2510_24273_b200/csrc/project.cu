@@ -42,6 +42,8 @@ project_kernel(ProjectArgs a) {
     // ---- role 2: RoPE of the query heads at position s_b - 1 (fp32 out) ----
     const int half = a.rope.half, d = 2 * half;
     const int nq = a.n_q;
+    if (a.hist0_zero)   // the score kernel accumulates the top-digit histogram into this
+      for (int i = rank * kProjThreads + tid; i < a.hist0_words; i += CS * kProjThreads) a.hist0_zero[i] = 0u;
     // (request, head, pair) tasks split over the CS CTAs of this row; loads of 8
     // tasks are issued before any math so the latency is paid once per batch
     const int per_req = half * nq;

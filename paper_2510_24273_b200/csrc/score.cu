@@ -24,6 +24,10 @@ latent_score_kernel(ScoreArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sub = lane / LG, li = lane % LG;
   const int V = a.rstar / EPC;  // 16-B chunks per token
+  __shared__ uint32_t hs[kH0Bins];
+  if (a.hist0)
+    for (int i = threadIdx.x; i < kH0Bins; i += kScoreThreads) hs[i] = 0;
+  __syncthreads();
 
   pdl_wait();
   float qreg[CPL][EPC];
@@ -40,6 +44,9 @@ latent_score_kernel(ScoreArgs a) {
   const size_t row_bytes = (size_t)a.r * sizeof(T);
   float* out = a.scores + (size_t)b * a.stride;
   constexpr int kWarps = kScoreThreads / 32;
+  // ranked range (global indices) for the top-digit histogram
+  const int64_t s_glob = a.hist0 ? a.seq_len[b] : 0;
+  const int64_t r_lo = a.sink, r_hi = s_glob - a.recent;
 
   for (int tb = t0 + warp * TPW * UNR; tb < t1; tb += kWarps * TPW * UNR) {
     uint4 raw[UNR][CPL];
@@ -67,13 +74,24 @@ latent_score_kernel(ScoreArgs a) {
 #pragma unroll
       for (int off = LG / 2; off > 0; off >>= 1) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], off);
     }
-    if (li == 0) {
+    // every lane of a token group holds the token's score after the butterfly:
+    // lane li writes (and histograms) the tokens u with u % LG == li, in parallel
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        const int t = tb + u * TPW + sub;
-        if (t < t1) out[t] = acc[u];
+    for (int u = 0; u < UNR; ++u) {
+      if (u % LG != li) continue;
+      const int t = tb + u * TPW + sub;
+      if (t < t1) {
+        out[t] = acc[u];
+        const int64_t g = a.idx_base + t;
+        if (a.hist0 && g >= r_lo && g < r_hi) atomicAdd(&hs[float_key(acc[u]) >> kH0Shift], 1u);
       }
     }
+  }
+  if (a.hist0) {
+    __syncthreads();
+    uint32_t* gh = a.hist0 + (size_t)b * kH0Bins;
+    for (int i = threadIdx.x; i < kH0Bins; i += kScoreThreads)
+      if (hs[i]) atomicAdd(&gh[i], hs[i]);
   }
   pdl_launch_dependents();
 }

@@ -2,21 +2,24 @@
 // with the sink / critical / recent policy and ties to the lower
 // index (reading R5).  One thread-block CLUSTER per request.
 //
-// Each CTA of the cluster loads a contiguous slice of the request's scores
-// into shared memory as order-preserving uint32 keys.  Four 8-bit radix
-// passes find the threshold key T (the need-th largest ranked key): per-warp
-// shared-memory histograms -> CTA histogram -> summed across the cluster
-// through DSMEM, and every CTA picks the same digit.  A final ordered
+// Each CTA of the cluster holds a contiguous slice of the request's scores in
+// shared memory as order-preserving uint32 keys.  The threshold key T (the
+// need-th largest ranked key) is found by radix selection; a final ordered
 // compaction writes, in ascending index order, every forced entry, every
-// ranked entry with key > T, and the first (need - #{key > T}) entries with
-// key == T (lowest indices first, counted across CTAs in rank order).
+// ranked entry with key > T and the first (need - #{key > T}) entries equal to
+// T.  Ordered work is done warp-wise on 32 consecutive entries at a time
+// (ballot + popc), so shared-memory accesses are conflict-free.
+//
+// This is the GENERIC kernel, used for K9 (global selection over the
+// all-gathered shard candidates): four 8-bit cluster-wide radix passes
+// (per-warp histograms pushed to every peer with DSMEM stores).  The decode
+// path (K4) and the shard-local selection (K8) use the histogram-assisted
+// kernel in topk_hist.cu.
 //
 // mode 0 (sals_decode): entry e is token e; forced = [0,x) u [s-z,s); the
 //   k-x-z best of [x, s-z) are ranked; all s tokens when s <= k.
 // mode 1 (sharded): entries carry global indices (cand_idx, or idx_base + e);
 //   only the ranked range [x, s-z) takes part; up to k-x-z are selected.
-//   Used for a shard's local candidates and for the global select (K9) over
-//   the all-gathered candidates, which arrive in ascending index order.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -25,8 +28,15 @@ namespace sals {
 constexpr int kTopkWarps = kTopkThreads / 32;
 constexpr int kMaxCluster = 16;
 
-// Inclusive scan of one value per thread across the 512-thread block; *total
-// receives the block-wide sum (same value in every thread).
+#ifdef SALS_TC_TRACE
+__device__ unsigned long long g_tk_trace[32];
+#define TK_STAMP(i) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_tk_trace[(i)] = clock64(); } while (0)
+#else
+#define TK_STAMP(i) do {} while (0)
+#endif
+
+// Inclusive scan of one value per thread across the block; *total receives the
+// block-wide sum (same value in every thread).
 __device__ __forceinline__ int block_incl_scan(int v, int* warp_tot, int* total = nullptr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -53,15 +63,58 @@ __device__ __forceinline__ int block_incl_scan(int v, int* warp_tot, int* total 
   return r;
 }
 
+// Exclusive prefix over the warps of per-warp counts wc[w][q0..q0+NQ) in place
+// (warp 0), totals into tot[q].  Caller synchronises before and after.
+template <int NQ>
+__device__ __forceinline__ void warp_counts_exclusive(int (*wc)[4], int q0, int* tot) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+#pragma unroll
+    for (int q = q0; q < q0 + NQ; ++q) {
+      const int v = lane < kTopkWarps ? wc[lane][q] : 0;
+      int incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int n = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += n;
+      }
+      if (lane < kTopkWarps) wc[lane][q] = incl - v;
+      if (lane == 31) tot[q] = incl;
+    }
+  }
+}
+
+// Warp-level digit search: lane l owns bins 255 - 8l - j (descending); find the
+// bin holding the rem-th largest and the count still needed inside it.
+__device__ __forceinline__ void warp_digit_search(const uint32_t* hist, int rem, int* s_digit, int* s_need) {
+  const int lane = threadIdx.x & 31;
+  int c8[8], tot = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) { c8[j] = (int)hist[255 - 8 * lane - j]; tot += c8[j]; }
+  int incl = tot;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int nb = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += nb;
+  }
+  int excl = incl - tot;
+  if (excl < rem && rem <= incl) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (excl < rem && rem <= excl + c8[j]) { *s_digit = 255 - 8 * lane - j; *s_need = rem - excl; }
+      excl += c8[j];
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kTopkThreads)
 topk_cluster_kernel(TopkArgs a) {
   extern __shared__ __align__(16) uint8_t tk_smem[];
-  // Cluster exchange is push-based: every CTA stores its values into a slot of
-  // EVERY peer's shared memory (fire-and-forget st.shared::cluster), so after
-  // the cluster barrier all reads are local.
-  __shared__ uint32_t inc_hist[2][kMaxCluster][256];   // [pass parity][source rank][digit]
+  __shared__ uint32_t inc_hist[2][kMaxCluster][256];   // generic path: [pass parity][source rank][digit]
   __shared__ uint32_t s_tot[256];
-  __shared__ int inc_cnt[kMaxCluster][4];              // [source rank]: ranked, definite, ties
+  __shared__ int inc_cnt[kMaxCluster][8];              // [source rank]: ranked, def, eq, def0, cand
+  __shared__ int wcnt[kTopkWarps][4];                   // per-warp counts -> exclusive warp bases
+  __shared__ int s_ctot[4];
   __shared__ int warp_tot[32];
   __shared__ int s_digit, s_need, s_nranked;
 
@@ -69,31 +122,35 @@ topk_cluster_kernel(TopkArgs a) {
   const int rank = (int)cluster_ctarank();
   const int b = blockIdx.x / CS;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t lt_mask = (1u << lane) - 1u;
   const int slice = a.slice;
   uint32_t* keys = reinterpret_cast<uint32_t*>(tk_smem);
   uint8_t* cls = tk_smem + (size_t)slice * 4;   // 0 none, 1 forced, 2 ranked
-  // global indices are only stored when they come from a candidate list
   const size_t gidx_off = ((size_t)slice * 5 + 15) / 16 * 16;
   int* gidx = a.cand_idx ? reinterpret_cast<int*>(tk_smem + gidx_off) : nullptr;
-  // per-warp digit histograms after the key / class / index arrays
   uint32_t (*whist)[256] = reinterpret_cast<uint32_t (*)[256]>(
       tk_smem + gidx_off + (a.cand_idx ? (size_t)slice * 4 : 0));
 
+  TK_STAMP(0);
   pdl_wait();
+  TK_STAMP(1);
   const int s = a.seq_len[b];
   const int n = a.n_entries ? a.n_entries[b] : (a.cand_idx ? a.n_const : s);
   const int e0 = rank * slice;
   const int nloc = max(0, min(slice, n - e0));
   const int x = a.sink, z = a.recent;
   const bool all_mode0 = (a.mode == 0) && (s <= a.k);
+  // warp w owns the ordered chunk [w0, w1) of the slice, processed 32 entries per round
+  const int wc = ((nloc + kTopkWarps - 1) / kTopkWarps + 31) / 32 * 32;
+  const int w0 = min(nloc, warp * wc), w1 = min(nloc, w0 + wc);
 
-  // ---- load slice -> keys / classes (4 independent loads in flight per thread) ----
+  // ---- load slice -> keys / classes (8 independent loads in flight per thread) ----
   int my_ranked = 0;
-  for (int i0 = tid; i0 < nloc; i0 += 4 * kTopkThreads) {
-    float sc[4];
-    int ix[4];
+  for (int i0 = tid; i0 < nloc; i0 += 8 * kTopkThreads) {
+    float sc[8];
+    int ix[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 8; ++u) {
       const int i = i0 + u * kTopkThreads;
       sc[u] = 0.f;
       ix[u] = -1;
@@ -106,7 +163,7 @@ topk_cluster_kernel(TopkArgs a) {
       }
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 8; ++u) {
       const int i = i0 + u * kTopkThreads;
       if (i >= nloc) continue;
       const int idx = ix[u];
@@ -122,134 +179,159 @@ topk_cluster_kernel(TopkArgs a) {
       my_ranked += (c == 2);
     }
   }
-  {
-    int tot;
-    block_incl_scan(my_ranked, warp_tot, &tot);
-    if (tid >= kTopkThreads - 32 && tid - (kTopkThreads - 32) < CS)
-      st_dsmem_u32(mapa_shared(smem_u32(&inc_cnt[rank][0]), tid - (kTopkThreads - 32)), (uint32_t)tot);
-  }
-  cluster_sync_all();
-  if (tid == 0) {
-    int nr = 0;
-    for (int c = 0; c < CS; ++c) nr += inc_cnt[c][0];
-    int nd = (a.mode == 0) ? (all_mode0 ? 0 : a.k - x - z) : (a.k - x - z);
-    s_nranked = nr;
-    s_need = max(0, min(nd, nr));
-  }
   __syncthreads();
-  const int n_ranked = s_nranked;
-  const int need = s_need;
-  __syncthreads();
+  TK_STAMP(2);
 
-  // ---- radix select of the threshold key T (4 x 8-bit passes) ------------
+  // Results of either selection path: threshold key T, ties taken (lowest
+  // indices first), and the cross-CTA counts that place this CTA's output.
   uint32_t T = 0xffffffffu;
   int need_eq = 0;
-  if (need == n_ranked && need > 0) {
-    T = 0u; need_eq = n_ranked;          // every ranked entry is selected
-  } else if (need > 0) {
-    uint32_t prefix = 0;
-    int rem = need;
-    for (int i = tid; i < kTopkWarps * 256; i += kTopkThreads) (&whist[0][0])[i] = 0;
-    __syncthreads();
-    for (int pass = 0; pass < 4; ++pass) {
-      const int shift = 24 - 8 * pass;
-      // per-warp histogram of the digit (shared-memory atomics; a fully conflicting
-      // warp costs ~32 cycles, cheaper than aggregating with match.any)
-      for (int i = tid; i < nloc; i += kTopkThreads) {
-        if (cls[i] != 2) continue;
-        const uint32_t key = keys[i];
-        if (pass > 0 && ((key ^ prefix) >> (shift + 8)) != 0) continue;
-        atomicAdd(&whist[warp][(key >> shift) & 255u], 1u);
-      }
-      __syncthreads();
-      if (tid < 256) {
-        uint32_t t = 0;
-#pragma unroll
-        for (int w = 0; w < kTopkWarps; ++w) { t += whist[w][tid]; whist[w][tid] = 0; }
-        const uint32_t addr = smem_u32(&inc_hist[pass & 1][rank][tid]);
-        for (int c = 0; c < CS; ++c) st_dsmem_u32(mapa_shared(addr, c), t);
-      }
-      cluster_sync_all();
-      if (tid < 256) {
-        uint32_t t = 0;
-        for (int c = 0; c < CS; ++c) t += inc_hist[pass & 1][c][tid];
-        s_tot[tid] = t;
-      }
-      __syncthreads();
-      if (warp == 0) {
-        // lane l owns digits 255 - 8l - j, j = 0..7 (descending)
-        int c8[8], tot = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) { c8[j] = (int)s_tot[255 - 8 * lane - j]; tot += c8[j]; }
-        int incl = tot;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const int nb = __shfl_up_sync(0xffffffffu, incl, off);
-          if (lane >= off) incl += nb;
-        }
-        int excl = incl - tot;
-        if (excl < rem && rem <= incl) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            if (excl < rem && rem <= excl + c8[j]) { s_digit = 255 - 8 * lane - j; s_need = rem - excl; }
-            excl += c8[j];
-          }
-        }
-      }
-      __syncthreads();
-      prefix |= (uint32_t)s_digit << shift;
-      rem = s_need;
+  int def_before = 0, eq_before = 0, def_total = 0, eq_total = 0, eq_local = 0;
+  {
+    // four cluster-wide 8-bit radix passes
+    {
+      int tot;
+      block_incl_scan(my_ranked, warp_tot, &tot);
+      if (tid < CS) st_dsmem_u32(mapa_shared(smem_u32(&inc_cnt[rank][0]), tid), (uint32_t)tot);
     }
-    T = prefix;
-    need_eq = rem;
+    cluster_sync_all();
+    if (tid == 0) {
+      int nr = 0;
+      for (int c = 0; c < CS; ++c) nr += inc_cnt[c][0];
+      int nd = (a.mode == 0) ? (all_mode0 ? 0 : a.k - x - z) : (a.k - x - z);
+      s_nranked = nr;
+      s_need = max(0, min(nd, nr));
+    }
+    __syncthreads();
+    const int n_ranked = s_nranked;
+    const int need = s_need;
+    __syncthreads();
+    T = 0xffffffffu;
+    need_eq = 0;
+    if (need == n_ranked && need > 0) {
+      T = 0u; need_eq = n_ranked;          // every ranked entry is selected
+    } else if (need > 0) {
+      uint32_t prefix = 0;
+      int rem = need;
+      for (int i = tid; i < kTopkWarps * 256; i += kTopkThreads) (&whist[0][0])[i] = 0;
+      __syncthreads();
+      for (int pass = 0; pass < 4; ++pass) {
+        const int shift = 24 - 8 * pass;
+        for (int i = tid; i < nloc; i += kTopkThreads) {
+          if (cls[i] != 2) continue;
+          const uint32_t key = keys[i];
+          if (pass > 0 && ((key ^ prefix) >> (shift + 8)) != 0) continue;
+          atomicAdd(&whist[warp][(key >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (tid < 256) {
+          uint32_t t = 0;
+#pragma unroll
+          for (int w = 0; w < kTopkWarps; ++w) { t += whist[w][tid]; whist[w][tid] = 0; }
+          const uint32_t addr = smem_u32(&inc_hist[pass & 1][rank][tid]);
+          for (int c = 0; c < CS; ++c) st_dsmem_u32(mapa_shared(addr, c), t);
+        }
+        cluster_sync_all();
+        if (tid < 256) {
+          uint32_t t = 0;
+          for (int c = 0; c < CS; ++c) t += inc_hist[pass & 1][c][tid];
+          s_tot[tid] = t;
+        }
+        __syncthreads();
+        if (warp == 0) warp_digit_search(s_tot, rem, &s_digit, &s_need);
+        __syncthreads();
+        prefix |= (uint32_t)s_digit << shift;
+        rem = s_need;
+        __syncthreads();
+      }
+      T = prefix;
+      need_eq = rem;
+    }
+    // per-CTA definite / tie counts, exchanged
+    {
+      int dcnt = 0, ecnt = 0;
+      for (int base = w0; base < w1; base += 32) {
+        const int i = base + lane;
+        bool d = false, e = false;
+        if (i < w1) {
+          const uint8_t c = cls[i];
+          d = (c == 1) || (c == 2 && keys[i] > T);
+          e = (c == 2 && keys[i] == T);
+        }
+        dcnt += __popc(__ballot_sync(0xffffffffu, d));
+        ecnt += __popc(__ballot_sync(0xffffffffu, e));
+      }
+      if (lane == 0) { wcnt[warp][2] = dcnt; wcnt[warp][3] = ecnt; }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int d = 0, e = 0;
+      for (int w = 0; w < kTopkWarps; ++w) { d += wcnt[w][2]; e += wcnt[w][3]; }
+      s_ctot[2] = d;
+      s_ctot[3] = e;
+    }
+    __syncthreads();
+    if (tid < CS) {
+      st_dsmem_u32(mapa_shared(smem_u32(&inc_cnt[rank][1]), tid), (uint32_t)s_ctot[2]);
+      st_dsmem_u32(mapa_shared(smem_u32(&inc_cnt[rank][2]), tid), (uint32_t)s_ctot[3]);
+    }
+    cluster_sync_all();
+    for (int c = 0; c < CS; ++c) {
+      const int dc = inc_cnt[c][1], ec = inc_cnt[c][2];
+      if (c < rank) { def_before += dc; eq_before += ec; }
+      def_total += dc; eq_total += ec;
+    }
+    eq_local = inc_cnt[rank][2];
   }
+  TK_STAMP(9);
 
-  // ---- ordered compaction ------------------------------------------------
-  const int run = (nloc + kTopkThreads - 1) / kTopkThreads;
-  const int i0 = min(nloc, tid * run), i1 = min(nloc, i0 + run);
-  int n_def = 0, n_eq = 0;
-  for (int i = i0; i < i1; ++i) {
-    const uint8_t c = cls[i];
-    if (c == 1 || (c == 2 && keys[i] > T)) ++n_def;
-    else if (c == 2 && keys[i] == T) ++n_eq;
-  }
-  int def_cta, eq_cta;
-  const int def_incl = block_incl_scan(n_def, warp_tot, &def_cta);
-  const int eq_incl = block_incl_scan(n_eq, warp_tot, &eq_cta);
-  if (tid >= kTopkThreads - 32 && tid - (kTopkThreads - 32) < CS) {
-    const int c = tid - (kTopkThreads - 32);
-    st_dsmem_u32(mapa_shared(smem_u32(&inc_cnt[rank][1]), c), (uint32_t)def_cta);
-    st_dsmem_u32(mapa_shared(smem_u32(&inc_cnt[rank][2]), c), (uint32_t)eq_cta);
-  }
-  cluster_sync_all();
-  int def_before = 0, eq_before = 0, def_total = 0, eq_total = 0;
-  for (int c = 0; c < CS; ++c) {
-    const int dc = inc_cnt[c][1];
-    const int ec = inc_cnt[c][2];
-    if (c < rank) { def_before += dc; eq_before += ec; }
-    def_total += dc; eq_total += ec;
-  }
-  const int eq_local = inc_cnt[rank][2];
+  // ---- ordered compaction (shared by both paths) ----------------------------
   const int take_local = max(0, min(need_eq - eq_before, eq_local));
   const int out_base = def_before + min(need_eq, eq_before);
   const int count = def_total + min(need_eq, eq_total);
-
-  int pos = out_base + (def_incl - n_def) + min(eq_incl - n_eq, take_local);
-  int eq_rank = eq_incl - n_eq;
+  {
+    int dcnt = 0, ecnt = 0;
+    for (int base = w0; base < w1; base += 32) {
+      const int i = base + lane;
+      bool d = false, e = false;
+      if (i < w1) {
+        const uint8_t c = cls[i];
+        d = (c == 1) || (c == 2 && keys[i] > T);
+        e = (c == 2 && keys[i] == T);
+      }
+      dcnt += __popc(__ballot_sync(0xffffffffu, d));
+      ecnt += __popc(__ballot_sync(0xffffffffu, e));
+    }
+    if (lane == 0) { wcnt[warp][2] = dcnt; wcnt[warp][3] = ecnt; }
+  }
+  __syncthreads();
+  warp_counts_exclusive<2>(wcnt, 2, s_ctot);
+  __syncthreads();
   int* out = a.sel_out + (size_t)b * a.sel_stride;
   int* out2 = a.sel_out2 ? a.sel_out2 + (size_t)b * a.sel_stride : nullptr;
   float* osc = a.sel_score ? a.sel_score + (size_t)b * a.sel_stride : nullptr;
-  for (int i = i0; i < i1; ++i) {
-    const uint8_t c = cls[i];
-    bool take = false;
-    if (c == 1 || (c == 2 && keys[i] > T)) take = true;
-    else if (c == 2 && keys[i] == T) { take = eq_rank < take_local; ++eq_rank; }
-    if (take) {
-      const int gi = gidx ? gidx[i] : (int)(a.idx_base + e0 + i);
-      out[pos] = gi;
-      if (out2) out2[pos] = gi;
-      if (osc) osc[pos] = key_float(keys[i]);
-      ++pos;
+  {
+    int rd = wcnt[warp][2], re = wcnt[warp][3];     // running definite / tie counts before the round
+    for (int base = w0; base < w1; base += 32) {
+      const int i = base + lane;
+      bool d = false, e = false;
+      if (i < w1) {
+        const uint8_t c = cls[i];
+        d = (c == 1) || (c == 2 && keys[i] > T);
+        e = (c == 2 && keys[i] == T);
+      }
+      const uint32_t dm = __ballot_sync(0xffffffffu, d), em = __ballot_sync(0xffffffffu, e);
+      const int db = rd + __popc(dm & lt_mask);      // definite entries before i in this CTA
+      const int eb = re + __popc(em & lt_mask);      // ties before i in this CTA
+      if (d || (e && eb < take_local)) {
+        const int pos = out_base + db + min(eb, take_local);
+        const int gi = gidx ? gidx[i] : (int)(a.idx_base + e0 + i);
+        out[pos] = gi;
+        if (out2) out2[pos] = gi;
+        if (osc) osc[pos] = key_float(keys[i]);
+      }
+      rd += __popc(dm);
+      re += __popc(em);
     }
   }
   if (rank == CS - 1) {
@@ -260,8 +342,19 @@ topk_cluster_kernel(TopkArgs a) {
     }
     if (tid == 0 && a.sel_count) a.sel_count[b] = count;
   }
+  TK_STAMP(10);
   cluster_sync_all();   // keep shared memory alive until every peer finished its DSMEM reads
+  TK_STAMP(11);
   pdl_launch_dependents();
 }
 
 }  // namespace sals
+
+extern "C" int sals_debug_topk_trace(unsigned long long* out) {
+#ifdef SALS_TC_TRACE
+  return (int)cudaMemcpyFromSymbol(out, sals::g_tk_trace, sizeof(sals::g_tk_trace));
+#else
+  (void)out;
+  return -1;
+#endif
+}

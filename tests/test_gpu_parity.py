@@ -90,6 +90,46 @@ def test_topk_ties_lower_index():
     assert sel.cpu().numpy().tolist() == [list(range(40))] * 2
 
 
+@pytest.mark.parametrize("s,npat,sink,recent,k", [
+    (5000, 7, 0, 0, 512),        # few distinct scores: threshold bin > survivor limit -> radix passes
+    (5000, 1000, 4, 64, 512),    # many distinct values: survivor select
+    (40000, 3, 0, 0, 4096),      # > candidate capacity: cluster-wide overflow passes
+    (131072, 2, 16, 128, 16384), # c4 geometry, two score values
+    (70001, 50000, 8, 32, 4096), # ragged, mostly distinct
+])
+def test_topk_exact_on_kernel_scores(s, npat, sink, recent, k):
+    """Selection is bit-exact given the scores: compare the kernel's C with the
+    oracle's select_topk (R3-R5) applied to the kernel's own p' (scores_out).
+    Latent rows are drawn from npat patterns so equal scores are frequent."""
+    from paper_2510_24273_b200 import sals
+    sh = _shape("c2", num_q_heads=4, num_kv_heads=4, rank=64, score_rank=32, top_k=k)
+    sh.update(sink=sink, recent=recent)
+    cfg = sals.make_config(**sh)
+    B = 2
+    g = torch.Generator(device="cuda"); g.manual_seed(7 + s + npat)
+    U = torch.from_numpy(synth.orthonormal(np.random.default_rng(1), 512, 64).astype(np.float32)).cuda().bfloat16()
+    pats = torch.randn(npat, 64, device="cuda", generator=g).bfloat16()
+    which = torch.randint(0, npat, (B, s), device="cuda", generator=g)
+    lat = pats[which].contiguous()
+    v = torch.randn(B, s, 512, device="cuda", generator=g).bfloat16()
+    q = torch.randn(B, 512, device="cuda", generator=g).bfloat16()
+    seq = torch.tensor([s, s - s // 3], dtype=torch.int32, device="cuda")
+    ws = sals.alloc_workspace(sals.sals_workspace_bytes(cfg, B, s), "cuda")
+    out = torch.empty(B, 512, dtype=torch.bfloat16, device="cuda")
+    sel = torch.empty(B, k, dtype=torch.int32, device="cuda")
+    scores = torch.empty(B, s, dtype=torch.float32, device="cuda")
+    sals.sals_decode(cfg, U, q, lat, v, seq, s, out, ws, sel_idx_out=sel, scores_out=scores)
+    torch.cuda.synchronize()
+    sc = scores.cpu().numpy()
+    got = sel.cpu().numpy()
+    for b in range(B):
+        sb = int(seq[b])
+        want = O.select_topk(sc[b, :sb].astype(np.float64), k, sink=sink, recent=recent)
+        n = len(want)
+        assert np.array_equal(got[b, :n], want), f"request {b}"
+        assert (got[b, n:] == -1).all()
+
+
 def test_graph_capture_replay_is_deterministic():
     from paper_2510_24273_b200 import sals
     sh = _shape("c3", rank=256, score_rank=128, top_k=512)
