@@ -7,7 +7,7 @@ hdr = rows[start]
 ik, iv = hdr.index("Kernel Name"), hdr.index("Metric Value")
 d = defaultdict(list)
 for r in rows[start + 1:]:
-    if len(r) > iv and ("sals" in r[ik]):
+    if len(r) > iv:
         d[r[ik].split("(")[0][:70]].append(float(r[iv].replace(",", "")) / 1e3)
 tot = 0
 for k, v in d.items():
