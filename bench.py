@@ -270,17 +270,12 @@ def run_sals(args, rank, world):
     ms = max_over_ranks(ms, world)
     value = world * B / (ms / 1e3)
 
-    # ---- per-stage timing (events on the launching stream), layer 0
-    with torch.cuda.stream(stream):
-        ly = layers[0]
-        stages = sals.sals_decode_profile(cfg, ly["U"], ly["q"], ly["latent"], ly["v"], seq, s, out[0], ws, iters=20)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(20):
-            sals.sals_append_latent(cfg, ly["U"], ly["k_new"], ly["v_new"], pos, ly["latent"], ly["v"])
-        e1.record(stream)
-        stream.synchronize()
-        stages["append"] = e0.elapsed_time(e1) / 20
+    # ---- per-stage timing, live: for each stage a CUDA graph of the same 32-layer step
+    # with only that stage's kernel enabled (sals_profile_stage_mask), replayed on the
+    # launching stream and timed with CUDA events; ms per launch = graph time / layers.
+    # Inputs are what the full step left in the workspace.  Back-to-back launches of one
+    # kernel overlap prologue/epilogue through PDL exactly as in the full step.
+    stages = stage_times(sals, step, stream, args, world, L)
     stages_us = {k: round(v * 1e3, 2) for k, v in stages.items() if v > 0}
 
     # ---- dense comparator (same build), same batch / layers
@@ -339,6 +334,29 @@ def run_sals(args, rank, world):
                                           f"shape (median {t_req:.3f} s), extrapolated x{B} requests x{L} layers"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def stage_times(sals, step, stream, args, world, L):
+    out = {}
+    with torch.cuda.stream(stream):
+        for name, bit in sals.STAGE_BITS.items():
+            sals.sals_profile_stage_mask(1 << bit)
+            try:
+                sals.sals_launch_count(reset=True)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    step()
+                n = sals.sals_launch_count(reset=True)
+            finally:
+                sals.sals_profile_stage_mask(0xffffffff)
+            if n == 0:
+                continue
+            step()   # a full step first: every stage's inputs valid (a stage-only replay may leave
+            ms = time_graph(g, stream, max(10, args.steps), 3, world)   # e.g. the histogram over-counted)
+            out[name] = max_over_ranks(ms, world) / n
+            del g
+            step()
+    return out
 
 
 def run_e2e(cfg, layers, seq, pos, s, ws, out, stream, args, world):

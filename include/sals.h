@@ -196,6 +196,14 @@ const char* sals_last_error(void);
 /* Number of kernel launches enqueued by the calling thread since the last reset
  * (bench.py's gpu_launches count). */
 uint64_t sals_launch_count(int32_t reset);
+/* Profiling only: restrict the calling thread's sals_decode / sals_append_latent
+ * to a subset of their kernels so a benchmark can time one stage in isolation
+ * (its inputs are whatever the previous full call left in the workspace).
+ * Bit 0 query projection + query RoPE, 1 latent scoring, 2 top-k,
+ * 3 reconstruct (+ fused attention on the tcgen05 path), 4 SIMT flash
+ * attention, 5 LSE merge, 6 sals_append_latent.  0xffffffff (the default)
+ * runs everything.  Returns the previous mask. */
+uint32_t sals_profile_stage_mask(uint32_t mask);
 
 #ifdef __cplusplus
 }

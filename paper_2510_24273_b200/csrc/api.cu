@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/sals.h"
@@ -26,6 +27,12 @@ struct StageTimer {
   bool used[kNumStages];
 };
 thread_local StageTimer* g_timer = nullptr;
+// Stage mask (sals_profile_stage_mask): bit i enables stage i; bit kNumStages the append.
+thread_local uint32_t g_stage_mask = 0xffffffffu;
+// TMA score kernel for bf16 (SALS_SCORE_LSU=1 in the environment selects the LSU kernel).
+const bool g_fused_merge = [] { const char* e = getenv("SALS_FUSED_MERGE"); return e && e[0] == '1'; }();
+const bool g_score_tma = [] { const char* e = getenv("SALS_SCORE_LSU"); return !(e && e[0] == '1'); }();
+inline bool on(int stage) { return (g_stage_mask >> stage) & 1u; }
 void mark_begin(cudaStream_t st) { if (g_timer) cudaEventRecord(g_timer->ev[kNumStages], st); }
 void mark(int stage, cudaStream_t st) {
   if (!g_timer) return;
@@ -141,6 +148,7 @@ struct Plan {
   int proj_cs, proj_rows;
   // workspace offsets
   size_t off_qtil, off_qrope, off_scores, off_sel, off_count, off_kr, off_part, off_hist, total;
+  int hist_words;          // histogram + (tcgen05 v2) split-merge counters, zeroed by the query projection
   int64_t score_stride;
 };
 
@@ -154,8 +162,10 @@ bool tc_eligible(const sals_config* c, int batch, int kmax) {
 // candidates (K9); else the histogram-assisted kernel (K4 / K8).
 constexpr size_t kTopkDynSmem = 190 * 1024;
 sals_status plan_topk(int n_entries, bool cand, Plan& p) {
+  static const int slice_env = [] { const char* e = getenv("SALS_TOPK_SLICE"); return e ? atoi(e) : 0; }();
+  const int target = (slice_env >= 256 && slice_env <= 16384) ? slice_env : 2048;   // experiment override
   int cs = 1;
-  while (cs < 16 && ceil_div(n_entries, cs) > 2048) cs <<= 1;
+  while (cs < 16 && ceil_div(n_entries, cs) > target) cs <<= 1;
   int slice = ceil_div(n_entries, cs);
   slice = (int)align_up(std::max(slice, 4), 4);
   const int cap = cand ? 16384 : 24576;
@@ -189,9 +199,16 @@ int flash_tpw_unr(const sals_config* c) {
   return (32 / lpt) * 2;
 }
 
-// Rows of U per CTA of the projection cluster: a multiple of 8 (16-byte vectors).
-void plan_proj(Plan& p) {
-  const int cs = std::min(16, std::max(1, ceil_div(p.D, 64)));
+// Rows of U per CTA of the projection cluster: a multiple of 8 (16-byte vectors),
+// at most 512.  Measured (bench stage times, c2 D = 4096 / c3 D = 1024): 8-CTA
+// clusters for the append (8 column blocks at r = 512) and for D <= 2048; the
+// query projection at D = 4096 (4 column blocks at r* = 256) prefers 16 (all
+// 256 rows of a CTA prefetched before the PDL wait).
+void plan_proj(Plan& p, bool query) {
+  static const int cs_env = [] { const char* e = getenv("SALS_PROJ_CS"); return e ? atoi(e) : 0; }();
+  int cs = std::min((query && p.D > 2048) ? 16 : 8, std::max(1, ceil_div(p.D, 64)));
+  while (ceil_div(p.D, cs) > 512) cs *= 2;
+  if (cs_env >= 1 && cs_env <= 16 && ceil_div(p.D, cs_env) <= 512) cs = cs_env;   // experiment override
   p.proj_rows = (int)align_up(ceil_div(p.D, cs), 8);
   p.proj_cs = ceil_div(p.D, p.proj_rows);
 }
@@ -219,7 +236,7 @@ sals_status make_plan(const sals_config* c, int batch, int max_s, Plan& p, bool 
   }
   sals_status st = plan_topk(max_s, false, p);
   if (st != SALS_OK) return st;
-  plan_proj(p);
+  plan_proj(p, true);
   const size_t es = esize(c);
   p.score_stride = (int64_t)align_up(max_s, 4);
   size_t off = 0;
@@ -231,7 +248,8 @@ sals_status make_plan(const sals_config* c, int batch, int max_s, Plan& p, bool 
   p.off_count = take((size_t)batch * 4);
   p.off_kr = take(p.tc ? 0 : (size_t)batch * c->top_k * p.D * es);
   p.off_part = take((size_t)batch * c->num_q_heads * p.nsplit * (c->head_dim + 2) * 4);
-  p.off_hist = take((size_t)batch * kH0Bins * 4);
+  p.hist_words = batch * kH0Bins + (p.tc2 ? batch * (p.D / 256) : 0);
+  p.off_hist = take((size_t)p.hist_words * 4);
   p.total = off;
   return SALS_OK;
 }
@@ -256,6 +274,17 @@ sals_status launch_project(const sals_config* c, const Plan& p, bool pool, Proje
 
 template <typename T>
 sals_status launch_score(const sals_config* c, ScoreArgs a, int batch, int max_len, cudaStream_t st) {
+  if (sizeof(T) == 2 && g_score_tma) {
+    static int nsm = 0;
+    if (!nsm) {
+      int dev = 0;
+      SALS_CUDA_TRY(cudaGetDevice(&dev));
+      SALS_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    cudaError_t e = launch_score_tma(a, batch, max_len, st, nsm);
+    if (e == cudaSuccess) { g_launches.fetch_add(1, std::memory_order_relaxed); return SALS_OK; }
+    if (e != cudaErrorNotSupported) return fail(SALS_ERR_CUDA, "score_tma launch: %s", cudaGetErrorString(e));
+  }
   const int epc = sizeof(T) == 2 ? 8 : 4;
   const int V = c->score_rank / epc;
   int LG, CPL;
@@ -372,26 +401,34 @@ sals_status attend_list(const sals_config* c, const Plan& p, const void* U, cons
     t.G = p.G; t.n_q = c->num_q_heads; t.pos_base = pos_base; t.rope = make_rope(c);
     t.qrope = qrope; t.scale_log2 = scale_log2(c); t.partials = part; t.ntiles = p.nsplit;
     t.tiles_per_cta = p.tc2 ? p.chunk : 0;
-    const bool direct = p.tc2 && p.nsplit == 1 && !partial_out;
+    // v2 writes y itself: directly for one chunk, else the last chunk CTA merges
+    // measured: the separate merge kernel beats the in-kernel last-CTA merge
+    // (SALS_FUSED_MERGE=1) at c3 / c4, so by default only a single chunk writes y directly
+    const bool direct = p.tc2 && !partial_out &&
+                        (p.nsplit == 1 || (g_fused_merge && p.nsplit <= tc2_merge_max_splits(p.G)));
     t.direct_out = direct ? out : nullptr;
-    sals_status s = launch_recon_attn_tc(t, batch, st);
-    if (s != SALS_OK) return fail(s, "%s", tc_last_error());
-    g_launches.fetch_add(1, std::memory_order_relaxed);
+    t.counters = (direct && p.nsplit > 1)
+                     ? reinterpret_cast<unsigned*>(ws + p.off_hist) + (size_t)batch * kH0Bins : nullptr;
+    if (on(kStReconAttn)) {
+      sals_status s = launch_recon_attn_tc(t, batch, st);
+      if (s != SALS_OK) return fail(s, "%s", tc_last_error());
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
     mark(kStReconAttn, st);
-    if (direct) return SALS_OK;   // y written by the fused kernel (single chunk per request)
+    if (direct) return SALS_OK;   // y written by the fused kernel
   } else {
     ReconArgs r{};
     r.latent = latent; r.cap = cap; r.r = c->rank; r.U = U; r.sel = sel; r.count = count;
     r.k_stride = c->top_k; r.D = p.D; r.head_dim = c->head_dim; r.pos_base = pos_base;
     r.rope = make_rope(c); r.kr = ws + p.off_kr;
-    sals_status s = launch_recon_simt<T>(c, r, batch, p.kmax, st);
+    sals_status s = on(kStReconAttn) ? launch_recon_simt<T>(c, r, batch, p.kmax, st) : SALS_OK;
     if (s != SALS_OK) return s;
     mark(kStReconAttn, st);
     FlashArgs f{};
     f.qrope = qrope; f.kbase = ws + p.off_kr; f.v_cache = v_cache; f.sel = sel; f.count = count;
     f.cap = cap; f.D = p.D; f.k_stride = c->top_k; f.n_q = c->num_q_heads; f.n_kv = c->num_kv_heads;
     f.nsplit = p.nsplit; f.chunk = p.chunk; f.scale_log2 = scale_log2(c); f.partials = part;
-    s = launch_flash<T, false>(c, f, batch, st);
+    s = on(kStFlash) ? launch_flash<T, false>(c, f, batch, st) : SALS_OK;
     if (s != SALS_OK) return s;
     mark(kStFlash, st);
   }
@@ -402,6 +439,7 @@ sals_status attend_list(const sals_config* c, const Plan& p, const void* U, cons
   m.nsplit = p.nsplit; m.n_q = c->num_q_heads; m.head_dim = c->head_dim;
   m.out = partial_out ? (void*)partial_out : out;
   m.normalize = partial_out ? 0 : 1;
+  if (!on(kStMerge)) return SALS_OK;
   sals_status ms = partial_out ? launch_merge<float>(c, m, batch, st) : launch_merge<T>(c, m, batch, st);
   mark(kStMerge, st);
   return ms;
@@ -424,9 +462,9 @@ sals_status decode_impl(const sals_config* c, const void* U, const void* q, cons
   pa.ncols = c->score_rank; pa.B = batch; pa.head_dim = c->head_dim; pa.group = p.G;
   pa.n_q = c->num_q_heads; pa.out_f32 = qtil; pa.qrope = qrope; pa.seq_len = seq_len; pa.rope = make_rope(c);
   uint32_t* hist = reinterpret_cast<uint32_t*>(ws + p.off_hist);
-  pa.hist0_zero = hist; pa.hist0_words = batch * kH0Bins;
+  pa.hist0_zero = hist; pa.hist0_words = p.hist_words;
   mark_begin(st);
-  sals_status s = launch_project<T>(c, p, true, pa, c->score_rank, st);
+  sals_status s = on(kStQproj) ? launch_project<T>(c, p, true, pa, c->score_rank, st) : SALS_OK;
   if (s != SALS_OK) return s;
   mark(kStQproj, st);
 
@@ -434,7 +472,7 @@ sals_status decode_impl(const sals_config* c, const void* U, const void* q, cons
   sa.latent = latent; sa.cap = cap; sa.r = c->rank; sa.rstar = c->score_rank; sa.qtil = qtil;
   sa.len = seq_len; sa.scores = scores; sa.stride = sstride;
   sa.hist0 = hist; sa.seq_len = seq_len; sa.idx_base = 0; sa.sink = c->sink; sa.recent = c->recent;
-  s = launch_score<T>(c, sa, batch, max_s, st);
+  s = on(kStScore) ? launch_score<T>(c, sa, batch, max_s, st) : SALS_OK;
   if (s != SALS_OK) return s;
   mark(kStScore, st);
 
@@ -444,7 +482,7 @@ sals_status decode_impl(const sals_config* c, const void* U, const void* q, cons
   ta.sel_out = sel; ta.sel_stride = c->top_k; ta.sel_count = count; ta.pad_to = c->top_k;
   ta.sel_out2 = sel_out;
   ta.hist0 = hist;
-  s = launch_topk(ta, batch, p, st);
+  s = on(kStTopk) ? launch_topk(ta, batch, p, st) : SALS_OK;
   if (s != SALS_OK) return s;
   mark(kStTopk, st);
 
@@ -469,6 +507,12 @@ const char* sals_status_string(sals_status s) {
 
 const char* sals_last_error(void) { return g_err.c_str(); }
 
+uint32_t sals_profile_stage_mask(uint32_t mask) {
+  const uint32_t old = g_stage_mask;
+  g_stage_mask = mask;
+  return old;
+}
+
 uint64_t sals_launch_count(int32_t reset) {
   return reset ? g_launches.exchange(0) : g_launches.load();
 }
@@ -490,12 +534,13 @@ sals_status sals_append_latent(const sals_config* cfg, const void* U, const void
   if (batch < 1 || batch > 65535 || cap < 1) return fail(SALS_ERR_INVALID_ARGUMENT, "bad batch / cap");
   Plan p{};
   p.D = cfg->num_kv_heads * cfg->head_dim;
-  plan_proj(p);
+  plan_proj(p, false);
   ProjectArgs a{};
   a.U = U; a.x = k_new; a.x_stride = p.D; a.D = p.D; a.r = cfg->rank; a.ncols = cfg->rank; a.B = batch;
   a.head_dim = cfg->head_dim; a.group = 1; a.n_q = cfg->num_q_heads; a.latent = latent_cache; a.cap = cap;
   a.pos = d_pos; a.v_new = v_new; a.v_cache = v_cache;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (!on(kNumStages)) return SALS_OK;
   if (cfg->dtype == SALS_BF16) return launch_project<__nv_bfloat16>(cfg, p, false, a, cfg->rank, st);
   return launch_project<float>(cfg, p, false, a, cfg->rank, st);
 }
@@ -660,7 +705,7 @@ sals_status sals_shard_candidates(const sals_config* cfg, const void* U, const v
   pa.out_f32 = qtil; pa.qrope = reinterpret_cast<float*>(ws + p.off_qrope); pa.seq_len = d_seq_len;
   pa.rope = make_rope(cfg);
   uint32_t* hist = reinterpret_cast<uint32_t*>(ws + p.off_hist);
-  pa.hist0_zero = hist; pa.hist0_words = batch * kH0Bins;
+  pa.hist0_zero = hist; pa.hist0_words = p.hist_words;
   ScoreArgs sa{};
   sa.latent = latent_shard; sa.cap = cap_local; sa.r = cfg->rank; sa.rstar = cfg->score_rank; sa.qtil = qtil;
   sa.len = d_local_len; sa.scores = scores; sa.stride = p.score_stride;

@@ -26,10 +26,13 @@ recon_rope_simt_kernel(ReconArgs a) {
   float* Bs = As + kRcRows * (kRcK + 1);        // [DH][33]
   float* Ks = Bs + DH * (kRcK + 1);             // [32][DH]
   __shared__ int rows[kRcRows];
+  __shared__ float2 sth[128];   // per-lane indexed: keep the angle table out of param space
   const int b = blockIdx.z, g = blockIdx.y, t0 = blockIdx.x * kRcRows;
   const int tid = threadIdx.x;
   const T* lat = reinterpret_cast<const T*>(a.latent);
   const T* U = reinterpret_cast<const T*>(a.U);
+  for (int i = tid; i < a.head_dim / 2; i += kRcThreads) sth[i] = make_float2(a.rope.th_hi[i], a.rope.th_lo[i]);
+  __syncthreads();
 
   pdl_wait();
   const int cnt = a.count[b];
@@ -78,7 +81,7 @@ recon_rope_simt_kernel(ReconArgs a) {
     const int row = rows[rr];
     if (row < 0) continue;
     int lo, hi; rope_pair(p, half, a.rope.style, lo, hi);
-    float c, s; rope_cs_fast(a.rope.th_hi[p], a.rope.th_lo[p], (int)(a.pos_base + row), c, s);
+    float c, s; rope_cs_fast(sth[p].x, sth[p].y, (int)(a.pos_base + row), c, s);
     const float xl = Ks[rr * DH + lo], xh = Ks[rr * DH + hi];
     T* dst = kr + ((size_t)b * a.k_stride + t0 + rr) * a.D + g * DH;
     dst[lo] = Elem<T>::from_f(xl * c - xh * s);
@@ -240,8 +243,61 @@ __global__ void merge_kernel(MergeArgs a) {
   const int b = bh / a.n_q, h = bh % a.n_q;
   pdl_wait();
   const float* base = a.partials + (size_t)bh * a.bh_stride;
+  constexpr int kMaxS = 512;
+  __shared__ float sw[kMaxS], sl[kMaxS];
+  __shared__ float s_M, s_L;
+  if (a.nsplit <= kMaxS) {
+    // (1) all (m, l) in one round of loads, (2) max and weights by warp 0,
+    // (3) y = sum_s w_s o_s with independent loads -- two dependent L2 round trips
+    for (int s = threadIdx.x; s < a.nsplit; s += blockDim.x) {
+      sw[s] = base[(size_t)s * a.s_stride];
+      sl[s] = base[(size_t)s * a.s_stride + 1];
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      float M = -INFINITY;
+      for (int s = threadIdx.x; s < a.nsplit; s += 32) M = fmaxf(M, sw[s]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+      float L = 0.f;
+      for (int s = threadIdx.x; s < a.nsplit; s += 32) {
+        const float ms = sw[s];
+        const float w = ms == -INFINITY ? 0.f : exp2f(ms - M);
+        sw[s] = w;
+        L = fmaf(sl[s], w, L);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+      if (threadIdx.x == 0) { s_M = M; s_L = L; }
+    }
+    __syncthreads();
+    const float M = s_M, L = s_L;
+    for (int i = threadIdx.x; i < a.head_dim; i += blockDim.x) {
+      const float* po = base + 2 + i;
+      float acc = 0.f;
+      int s = 0;
+      for (; s + 8 <= a.nsplit; s += 8) {
+        float ov[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) ov[j] = po[(size_t)(s + j) * a.s_stride];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc = fmaf(sw[s + j], ov[j], acc);
+      }
+      for (; s < a.nsplit; ++s) acc = fmaf(sw[s], po[(size_t)s * a.s_stride], acc);
+      if (a.normalize) {
+        T* out = reinterpret_cast<T*>(a.out) + ((size_t)b * a.n_q + h) * a.head_dim;
+        out[i] = Elem<T>::from_f(L > 0.f ? acc / L : 0.f);
+      } else {   // un-normalised partial (M, L, O) for the cross-rank merge
+        float* out = reinterpret_cast<float*>(a.out) + (size_t)bh * (a.head_dim + 2);
+        out[2 + i] = acc;
+        if (i == 0) { out[0] = M; out[1] = L; }
+      }
+    }
+    pdl_launch_dependents();
+    return;
+  }
   for (int i = threadIdx.x; i < a.head_dim; i += blockDim.x) {
-    // one pass over the splits with a running max (independent loads, no dependent phases)
+    // many splits: one pass with a running max
     float M = -INFINITY, L = 0.f, acc = 0.f;
 #pragma unroll 4
     for (int s = 0; s < a.nsplit; ++s) {
@@ -257,7 +313,7 @@ __global__ void merge_kernel(MergeArgs a) {
     if (a.normalize) {
       T* out = reinterpret_cast<T*>(a.out) + ((size_t)b * a.n_q + h) * a.head_dim;
       out[i] = Elem<T>::from_f(L > 0.f ? acc / L : 0.f);
-    } else {   // un-normalised partial (M, L, O) for the cross-rank merge
+    } else {
       float* out = reinterpret_cast<float*>(a.out) + (size_t)bh * (a.head_dim + 2);
       out[2 + i] = acc;
       if (i == 0) { out[0] = M; out[1] = L; }
@@ -274,6 +330,9 @@ template __global__ void merge_kernel<__nv_bfloat16>(MergeArgs);
 template <typename T>
 __global__ void dense_append_kernel(DenseAppendArgs a) {
   const int b = blockIdx.x;
+  __shared__ float2 sth[128];   // per-lane indexed: keep the angle table out of param space
+  for (int i = threadIdx.x; i < a.head_dim / 2; i += blockDim.x) sth[i] = make_float2(a.rope.th_hi[i], a.rope.th_lo[i]);
+  __syncthreads();
   pdl_wait();
   const int64_t pos = a.pos[b];
   const T* k = reinterpret_cast<const T*>(a.k_new) + (size_t)b * a.D;
@@ -284,7 +343,7 @@ __global__ void dense_append_kernel(DenseAppendArgs a) {
   for (int t = threadIdx.x; t < a.n_kv * half; t += blockDim.x) {
     const int g = t / half, p = t % half;
     int lo, hi; rope_pair(p, half, a.rope.style, lo, hi);
-    float c, s; rope_cs_fast(a.rope.th_hi[p], a.rope.th_lo[p], (int)pos, c, s);
+    float c, s; rope_cs_fast(sth[p].x, sth[p].y, (int)pos, c, s);
     const float xl = Elem<T>::to_f(k[g * a.head_dim + lo]), xh = Elem<T>::to_f(k[g * a.head_dim + hi]);
     kc[g * a.head_dim + lo] = Elem<T>::from_f(xl * c - xh * s);
     kc[g * a.head_dim + hi] = Elem<T>::from_f(xl * s + xh * c);

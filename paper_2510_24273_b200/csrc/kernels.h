@@ -118,6 +118,8 @@ struct OwnedArgs {        // sharded: owned selection list = owned sinks | owned
 
 template <typename T, bool POOL> __global__ void project_kernel(ProjectArgs a);
 template <typename T, int LG, int CPL> __global__ void latent_score_kernel(ScoreArgs a);
+// TMA-streamed bf16 scoring (score_tma.cu); cudaErrorNotSupported outside its shapes.
+cudaError_t launch_score_tma(const ScoreArgs& a, int batch, int max_len, cudaStream_t st, int nsm);
 __global__ void topk_cluster_kernel(TopkArgs a);
 template <int NT> __global__ void topk_hist_kernel(TopkArgs a);
 template <typename T> __global__ void recon_rope_simt_kernel(ReconArgs a);

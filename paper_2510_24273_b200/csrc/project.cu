@@ -20,9 +20,13 @@ constexpr int kProjWarps = kProjThreads / 32;
 constexpr int kProjBT = 8;        // requests per pass
 constexpr int kProjMaxRows = 512; // rows per CTA (D / CS)
 constexpr int kProjUnroll = 8;    // row loads in flight per lane
+constexpr int kProjPre = 8;       // rows per lane prefetched before griddepcontrol.wait (256 rows per CTA)
 
+#ifndef SALS_PROJ_MINB
+#define SALS_PROJ_MINB 1   // measured: an uncapped register budget (no spills) beats co-residence
+#endif
 template <typename T, bool POOL>
-__global__ void __launch_bounds__(kProjThreads)
+__global__ void __launch_bounds__(kProjThreads, SALS_PROJ_MINB)   // 2: <= 128 registers, co-resident with the next kernel
 project_kernel(ProjectArgs a) {
   constexpr int EPC = Elem<T>::kPer16;       // columns per lane
   constexpr int CPB = 8 * EPC;               // columns per CTA
@@ -36,9 +40,39 @@ project_kernel(ProjectArgs a) {
   const T* U = reinterpret_cast<const T*>(a.U);
   const T* x = reinterpret_cast<const T*>(a.x);
 
-  pdl_wait();
+  const int rows_per = a.rows_per_cta;
+  const int row0 = rank * rows_per;
+  const int row1 = min(a.D, row0 + rows_per);
+  const int slot = lane >> 3;                       // row slot 0..3 within a warp step
+  const int cl = lane & 7;                          // column vector within the CTA's block
+  const int col = blockIdx.y * CPB + cl * EPC;
+  const bool col_ok = col < a.ncols;
+  const char* Ub = reinterpret_cast<const char*>(U);
+  const size_t row_bytes = (size_t)a.r * sizeof(T);
+  const bool rope_role = POOL && blockIdx.y == gridDim.y - 1;
+  // U is a weight no upstream kernel writes: issue this lane's first (for
+  // D <= 16 * 256 its only) batch of U rows BEFORE waiting on the upstream
+  // grid, and keep them in registers for every request pass.
+  const int base0 = row0 + 4 * warp + slot;
+  uint4 pre[kProjPre];
+#pragma unroll
+  for (int u = 0; u < kProjPre; ++u) {
+    const int c = base0 + u * 4 * kProjWarps;
+    pre[u] = (!rope_role && col_ok && c < row1) ? ld_nc_v4(Ub + (size_t)c * row_bytes + col * sizeof(T))
+                                                : make_uint4(0, 0, 0, 0);
+  }
+  __shared__ float2 sth[128];   // (th_hi, th_lo) per rotation pair: indexed per lane, so not from param space
+  if (rope_role)
+    for (int i = tid; i < a.rope.half; i += kProjThreads) sth[i] = make_float2(a.rope.th_hi[i], a.rope.th_lo[i]);
+  __syncthreads();
 
-  if (POOL && blockIdx.y == gridDim.y - 1) {
+  pdl_wait();
+  // Dependents may launch now: their pre-wait sections only read weights (U) and
+  // the latent rows of earlier steps / of the sals_append_latent that this
+  // grid's griddepcontrol.wait has just seen complete (PDL).
+  pdl_launch_dependents();
+
+  if (rope_role) {
     // ---- role 2: RoPE of the query heads at position s_b - 1 (fp32 out) ----
     const int half = a.rope.half, d = 2 * half;
     const int nq = a.n_q;
@@ -67,7 +101,7 @@ project_kernel(ProjectArgs a) {
         const int t = t0 + u * CS * kProjThreads;
         if (t < total) {
           const int b = t / per_req, r = t % per_req, p = r % half, h = r / half;
-          float c, s; rope_cs_fast(a.rope.th_hi[p], a.rope.th_lo[p], a.seq_len[b] - 1, c, s);
+          float c, s; rope_cs_fast(sth[p].x, sth[p].y, a.seq_len[b] - 1, c, s);
           a.qrope[((size_t)b * nq + h) * d + lo_[u]] = xl[u] * c - xh[u] * s;
           a.qrope[((size_t)b * nq + h) * d + hi_[u]] = xl[u] * s + xh[u] * c;
         }
@@ -89,16 +123,6 @@ project_kernel(ProjectArgs a) {
                                 (((size_t)b * a.cap + a.pos[b]) * a.D) * sizeof(T) + v * 16) = val;
     }
   }
-
-  const int rows_per = a.rows_per_cta;
-  const int row0 = rank * rows_per;
-  const int row1 = min(a.D, row0 + rows_per);
-  const int slot = lane >> 3;                       // row slot 0..3 within a warp step
-  const int cl = lane & 7;                          // column vector within the CTA's block
-  const int col = blockIdx.y * CPB + cl * EPC;
-  const bool col_ok = col < a.ncols;
-  const char* Ub = reinterpret_cast<const char*>(U);
-  const size_t row_bytes = (size_t)a.r * sizeof(T);
 
   for (int b0 = 0; b0 < a.B; b0 += kProjBT) {
     const int nb = min(kProjBT, a.B - b0);
@@ -138,8 +162,23 @@ project_kernel(ProjectArgs a) {
 #pragma unroll
       for (int e = 0; e < EPC; ++e) acc[bb][e] = 0.f;
     if (col_ok) {
-      // rows handled by this lane: row0 + 4*(warp + 8*i) + slot
-      for (int base = row0 + 4 * warp + slot; base < row1; base += 4 * kProjWarps * kProjUnroll) {
+      // rows handled by this lane: base0 + 32 i (i < kProjPre from the prefetch, then streamed)
+      auto fma_row = [&](const uint4& raw, int c) {
+        float uf[EPC];
+        Elem<T>::unpack(raw, uf);
+#pragma unroll
+        for (int bb = 0; bb < kProjBT; ++bb) {
+          const float xv = xs[bb][c - row0];
+#pragma unroll
+          for (int e = 0; e < EPC; ++e) acc[bb][e] = fmaf(uf[e], xv, acc[bb][e]);
+        }
+      };
+#pragma unroll
+      for (int u = 0; u < kProjPre; ++u) {
+        const int c = base0 + u * 4 * kProjWarps;
+        if (c < row1) fma_row(pre[u], c);
+      }
+      for (int base = base0 + kProjPre * 4 * kProjWarps; base < row1; base += 4 * kProjWarps * kProjUnroll) {
         uint4 raw[kProjUnroll];
 #pragma unroll
         for (int u = 0; u < kProjUnroll; ++u) {
@@ -149,16 +188,7 @@ project_kernel(ProjectArgs a) {
 #pragma unroll
         for (int u = 0; u < kProjUnroll; ++u) {
           const int c = base + u * 4 * kProjWarps;
-          if (c < row1) {
-            float uf[EPC];
-            Elem<T>::unpack(raw[u], uf);
-#pragma unroll
-            for (int bb = 0; bb < kProjBT; ++bb) {
-              const float xv = xs[bb][c - row0];
-#pragma unroll
-              for (int e = 0; e < EPC; ++e) acc[bb][e] = fmaf(uf[e], xv, acc[bb][e]);
-            }
-          }
+          if (c < row1) fma_row(raw[u], c);
         }
       }
     }

@@ -425,6 +425,8 @@ bool tc_supported(int head_dim, int D, int rank, int G) {
 
 const char* tc_last_error() { return g_tc_err.c_str(); }
 
+void* tma_encoder_fn() { return get_encoder() ? reinterpret_cast<void*>(g_encode) : nullptr; }
+
 sals_status launch_recon_attn_tc(const TcArgs& a, int batch, cudaStream_t st) {
   if (!tc_supported(a.head_dim, a.D, a.r, a.G)) { g_tc_err = "shape not supported by the tcgen05 path"; return SALS_ERR_UNSUPPORTED; }
   if (!get_encoder()) { g_tc_err = "cuTensorMapEncodeTiled unavailable"; return SALS_ERR_CUDA; }

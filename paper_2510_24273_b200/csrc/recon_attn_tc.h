@@ -20,12 +20,18 @@ struct TcArgs {
   float* partials;        // [B, n_q, ntiles, d+2]
   int ntiles;             // v1: tiles per request = ceil(k / 128); v2: chunks per request
   int tiles_per_cta;      // v2: tiles of 128 tokens per CTA (chunk length)
-  void* direct_out;       // v2 with one chunk: write y [B, n_q*d] directly (no merge kernel)
+  void* direct_out;       // v2: write y [B, n_q*d] directly (no merge kernel): one chunk, or
+                          // several with `counters` (the last chunk CTA of a (request, column
+                          // block) merges the partials, deterministic split order)
+  unsigned* counters;     // v2, nullable: [B, D/256] arrival counters, zero on entry
 };
 
 bool tc_supported(int head_dim, int D, int rank, int G);
 bool tc2_supported(int head_dim, int D, int rank, int G);   // persistent v2 (d = 128, G <= 4)
+int tc2_merge_max_splits(int G);                             // in-kernel split merge limit
 sals_status launch_recon_attn_tc(const TcArgs& a, int batch, cudaStream_t st);
 const char* tc_last_error();
+// cuTensorMapEncodeTiled (driver entry point, resolved once), or nullptr.
+void* tma_encoder_fn();
 
 }  // namespace sals

@@ -32,10 +32,14 @@ constexpr int kThreads = 512;
 constexpr int kABytes = kRows * kBK * 2;   // 16 KB
 constexpr int kBBytes = kBN * kBK * 2;     // 32 KB
 constexpr int kVBytes = kRows * kBN * 2;   // 64 KB
+constexpr int kPS = kRows + 4;             // sP row stride (floats): the two KV-head halves of a warp hit different banks
 
+__host__ __device__ constexpr int smem_bytes(int G);
+static_assert(1024 + 3 * (128 * 64 * 2 + 256 * 64 * 2) + 128 * 256 * 2 + 8 * 64 * 8 + 16 * 128 * 4 + 8 * (128 + 4) * 4 + 1024 <=
+                  232448, "G = 4 shared memory over the 227 KB limit");
 __host__ __device__ constexpr int smem_bytes(int G) {
   return 1024 + kStages * (kABytes + kBBytes) + kVBytes + 2 * G * 64 * 8 /*sQ*/ + 2 * 2 * G * kRows * 4 /*sL*/ +
-         2 * G * kRows * 4 /*sP*/ + 2048 /*misc*/;
+         2 * G * kPS * 4 /*sP*/ + 1024 /*misc: sRed, sAl, sIdxV, barriers, TMEM slot (< 1 KB)*/;
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -137,11 +141,76 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void tmem_ld8_nowait(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+template <int N>
+__device__ __forceinline__ void tmem_ldn_nowait(uint32_t taddr, float* v) {
+  if constexpr (N == 16) tmem_ld16_nowait(taddr, v); else tmem_ld8_nowait(taddr, v);
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 struct KArgs {
   TcArgs a;
 };
+
+// Split merge fused into the kernel: every chunk CTA of (request b, column block
+// nb) has written its (m, l, o) partials and fenced them; the CTA that arrives
+// last merges the gridDim.x partials of its NQH query heads in split order
+// (log-sum-exp, two passes: max, then weighted sums) and writes y.  All threads
+// of the CTA call this.
+template <int NQH>
+__device__ __forceinline__ void merge_if_last(const TcArgs& a, int b, int nb, int tid, float* scratch) {
+  __shared__ int s_last;
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned old = atomicAdd(&a.counters[(size_t)b * gridDim.y + nb], 1u);   // after the partials' fences
+    s_last = old == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (tid == 0) a.counters[(size_t)b * gridDim.y + nb] = 0;   // every chunk CTA has arrived: re-arm
+  const int ns = gridDim.x;
+  // the NQH heads' partials [NQH][ns][d+2] are one contiguous block: stage it in
+  // shared memory with a single round of independent 8-byte loads, then merge
+  // (log-sum-exp, split order) from shared memory
+  const int blk = NQH * ns * (kDH + 2);
+  const float2* src = reinterpret_cast<const float2*>(a.partials + ((size_t)b * a.n_q + nb * NQH) * ns * (kDH + 2));
+  float2* dst = reinterpret_cast<float2*>(scratch);
+  for (int i = tid; i < blk / 2; i += kThreads) dst[i] = __ldcg(src + i);
+  float* sw = scratch + blk;          // [NQH][ns] normalised weights
+  __syncthreads();
+  if (tid < NQH) {
+    const float* ph = scratch + tid * ns * (kDH + 2);
+    float M = -INFINITY;
+    for (int sp = 0; sp < ns; ++sp) M = fmaxf(M, ph[sp * (kDH + 2)]);
+    float L = 0.f;
+    for (int sp = 0; sp < ns; ++sp) {
+      const float ms = ph[sp * (kDH + 2)];
+      const float w = ms == -INFINITY ? 0.f : exp2f(ms - M);
+      sw[tid * ns + sp] = w;
+      L = fmaf(ph[sp * (kDH + 2) + 1], w, L);
+    }
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    for (int sp = 0; sp < ns; ++sp) sw[tid * ns + sp] *= inv;
+  }
+  __syncthreads();
+  for (int o = tid; o < NQH * kDH; o += kThreads) {
+    const int qh = o / kDH, n = o - qh * kDH;
+    const float* ph = scratch + qh * ns * (kDH + 2) + 2 + n;
+    const float* w = sw + qh * ns;
+    float acc = 0.f;
+    for (int sp = 0; sp < ns; ++sp) acc = fmaf(w[sp], ph[sp * (kDH + 2)], acc);
+    __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(a.direct_out) + ((size_t)b * a.n_q + nb * NQH + qh) * kDH;
+    y[n] = __float2bfloat16_rn(acc);
+  }
+}
 
 #ifdef SALS_TC_TRACE
 __device__ unsigned long long g_trace[128];
@@ -168,9 +237,10 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
   uint8_t* sV = sB + kStages * kBBytes;
   float2* sQ = reinterpret_cast<float2*>(sV + kVBytes);          // [NQH][64] (q_lo, q_hi) per pair
   float* sL = reinterpret_cast<float*>(sQ + NQH * 64);           // [2 halves][NQH][128] partial logits
-  float* sP = sL + 2 * NQH * kRows;                              // [NQH][128] probabilities
-  float* sRed = sP + NQH * kRows;                                // [2 kinds][2 halves][4][G]
-  int* sIdxV = reinterpret_cast<int*>(sRed + 2 * 2 * 4 * G);     // [128] global rows of the V tile
+  float* sP = sL + 2 * NQH * kRows;                              // [NQH][kPS] probabilities
+  float* sRed = sP + NQH * kPS;                                  // [2 kinds][2 halves][4][G]
+  float* sAl = sRed + 2 * 2 * 4 * G;                             // [NQH] online-softmax rescale of the tile
+  int* sIdxV = reinterpret_cast<int*>(sAl + NQH);                // [128] global rows of the V tile
   uint64_t* bars = reinterpret_cast<uint64_t*>(sIdxV + kRows);
   uint64_t* full = bars;                 // [stages]
   uint64_t* empty = bars + kStages;      // [stages]
@@ -193,13 +263,13 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
   const int ntile = max(0, t_end - t_begin);
   const int* selb = a.sel + (size_t)b * a.k_stride;
 
-  if (ntile == 0) {   // no selected tokens for this chunk: empty partials
-    if (tid < NQH) {
-      const int h = nb * NQH + tid;
-      float* dst = a.partials + (((size_t)b * a.n_q + h) * a.ntiles + chunk) * (kDH + 2);
-      dst[0] = -INFINITY;
-      dst[1] = 0.f;
+  if (ntile == 0) {   // no selected tokens for this chunk: empty partials (m = -inf, l = 0, o = 0)
+    for (int i = tid; i < NQH * (kDH + 2); i += kThreads) {
+      const int qh = i / (kDH + 2), j = i - qh * (kDH + 2);
+      a.partials[(((size_t)b * a.n_q + nb * NQH + qh) * a.ntiles + chunk) * (kDH + 2) + j] = j == 0 ? -INFINITY : 0.f;
     }
+    if (a.counters) __threadfence();
+    if (a.counters) merge_if_last<NQH>(a, b, nb, tid, reinterpret_cast<float*>(smem));
     pdl_launch_dependents();
     return;
   }
@@ -336,10 +406,18 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
     // ================= epilogue =================
     const int ew = warp - 8, rq = warp & 3, hf = ew >> 2;
     const int m = rq * 32 + lane;                  // token row of the tile (TMEM lane)
-    const int n = rq * 32 + lane;                  // dim of KV head hf owned in P V
-    float m_run[G], l_run[G], o[G];
+    const int n = rq * 32 + lane;                  // dim of KV head hf in the final write
+    // P V mapping: warp ew owns tokens [16 ew, 16 ew + 16) of every tile; lane owns
+    // dims [8 (lane & 15), +8) of KV head kh = lane >> 4 (one 16-B V vector per token)
+    const int kh = lane >> 4;
+    float m_run[G], l_run[G];
+    float2 ov[G][4];
 #pragma unroll
-    for (int g = 0; g < G; ++g) { m_run[g] = -INFINITY; l_run[g] = 0.f; o[g] = 0.f; }
+    for (int g = 0; g < G; ++g) {
+      m_run[g] = -INFINITY; l_run[g] = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) ov[g][e] = make_float2(0.f, 0.f);
+    }
     const uint32_t tl = tmem + ((uint32_t)(rq * 32) << 16);
     for (int it = 0; it < ntile; ++it) {
       const int tile = t_begin + it, buf = it & 1;
@@ -356,40 +434,42 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
         for (int g = 0; g < G; ++g) part[j][g] = make_float2(0.f, 0.f);
       const uint32_t tacc = tl + buf * kBN;
       const float4* sQ4 = reinterpret_cast<const float4*>(sQ);
+      // pairs per TMEM chunk: 8 for G = 4 (register pressure), else 16
+      constexpr int PW = G >= 4 ? 8 : 16;
 #pragma unroll 1
-      for (int pc = 0; pc < 2; ++pc) {
-        const int p0 = 32 * hf + 16 * pc;
-        float xl[2][16], xh[2][16];
+      for (int pc = 0; pc < 32 / PW; ++pc) {
+        const int p0 = 32 * hf + PW * pc;
+        float xl[2][PW], xh[2][PW];
         // issue all four TMEM loads of the chunk, one wait
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           if (STYLE == 0) {
-            tmem_ld16_nowait(tacc + j * kDH + p0, xl[j]);
-            tmem_ld16_nowait(tacc + j * kDH + 64 + p0, xh[j]);
+            tmem_ldn_nowait<PW>(tacc + j * kDH + p0, xl[j]);
+            tmem_ldn_nowait<PW>(tacc + j * kDH + 64 + p0, xh[j]);
           } else {
-            tmem_ld16_nowait(tacc + j * kDH + 2 * p0, xl[j]);
-            tmem_ld16_nowait(tacc + j * kDH + 2 * p0 + 16, xh[j]);
+            tmem_ldn_nowait<PW>(tacc + j * kDH + 2 * p0, xl[j]);
+            tmem_ldn_nowait<PW>(tacc + j * kDH + 2 * p0 + PW, xh[j]);
           }
         }
-        float cs[16], sn[16];
+        float cs[PW], sn[PW];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) rope_cs_fast(a.rope.th_hi[p0 + i], a.rope.th_lo[p0 + i], pos, cs[i], sn[i]);
+        for (int i = 0; i < PW; ++i) rope_cs_fast(a.rope.th_hi[p0 + i], a.rope.th_lo[p0 + i], pos, cs[i], sn[i]);
         tmem_wait_ld();
         if (STYLE == 1) {   // de-interleave (2i, 2i+1) pairs
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
-            float t0[16], t1[16];
+            float t0[PW], t1[PW];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) { t0[i] = xl[j][i]; t1[i] = xh[j][i]; }
+            for (int i = 0; i < PW; ++i) { t0[i] = xl[j][i]; t1[i] = xh[j][i]; }
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 0; i < PW / 2; ++i) {
               xl[j][i] = t0[2 * i]; xh[j][i] = t0[2 * i + 1];
-              xl[j][8 + i] = t1[2 * i]; xh[j][8 + i] = t1[2 * i + 1];
+              xl[j][PW / 2 + i] = t1[2 * i]; xh[j][PW / 2 + i] = t1[2 * i + 1];
             }
           }
         }
 #pragma unroll
-        for (int i = 0; i < 16; i += 2) {
+        for (int i = 0; i < PW; i += 2) {
           const float2 c2 = make_float2(cs[i], cs[i + 1]);
           const float2 s2 = make_float2(sn[i], sn[i + 1]);
           const float2 ns2 = make_float2(-sn[i], -sn[i + 1]);
@@ -435,7 +515,7 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
         mnew[g] = fmaxf(m_run[g], mt);
         alpha[g] = exp2f(m_run[g] - mnew[g]);        // m_run = -inf -> 0
         const float p = (row >= 0) ? exp2f(lg[g] - mnew[g]) : 0.f;
-        sP[(hf * G + g) * kRows + m] = p;
+        sP[(hf * G + g) * kPS + m] = p;
         float v = p;
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
@@ -448,46 +528,73 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
         const float lt = (r[0] + r[G]) + (r[2 * G] + r[3 * G]);
         l_run[g] = l_run[g] * alpha[g] + lt;
         m_run[g] = mnew[g];
-        o[g] *= alpha[g];
+        if (rq == 0 && lane == 0) sAl[hf * G + g] = alpha[g];
       }
+      bar_epi();                                       // sP / sAl of both halves visible
       mbar_wait(vfull, it & 1);
       if (ew == 0 && lane == 0) TSTAMP(32 + it);
-      // ---- P V over the staged rows: dim n of KV head hf
-      const unsigned short* vcol = reinterpret_cast<const unsigned short*>(sV) + hf * kDH + n;
-      const float* pp = sP + hf * G * kRows;
-      float2 oa[G], ob[G];
-#pragma unroll
-      for (int g = 0; g < G; ++g) oa[g] = ob[g] = make_float2(0.f, 0.f);
-      int t = 0;
-#pragma unroll 2
-      for (; t + 4 <= nv; t += 4) {
-        const float2 va = make_float2(__uint_as_float((uint32_t)vcol[t * kBN] << 16),
-                                      __uint_as_float((uint32_t)vcol[(t + 1) * kBN] << 16));
-        const float2 vb = make_float2(__uint_as_float((uint32_t)vcol[(t + 2) * kBN] << 16),
-                                      __uint_as_float((uint32_t)vcol[(t + 3) * kBN] << 16));
+      // ---- P V: 16 tokens of this warp x 8 dims of KV head kh per lane, one 16-B V vector per token
+      {
+        float al[G];
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-          const float4 p4 = *reinterpret_cast<const float4*>(pp + g * kRows + t);
-          oa[g] = __ffma2_rn(make_float2(p4.x, p4.y), va, oa[g]);
-          ob[g] = __ffma2_rn(make_float2(p4.z, p4.w), vb, ob[g]);
+          al[g] = sAl[kh * G + g];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) { ov[g][e].x *= al[g]; ov[g][e].y *= al[g]; }
+        }
+        const uint4* vrow = reinterpret_cast<const uint4*>(sV) + lane;   // row t at vrow[t * 32]
+        const float* pp = sP + kh * G * kPS;
+        const int tb = 16 * ew;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const int t0 = tb + 4 * q4;
+          if (t0 >= nv) break;
+          float4 p4[G];
+#pragma unroll
+          for (int g = 0; g < G; ++g) p4[g] = *reinterpret_cast<const float4*>(pp + g * kPS + t0);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (t0 + j < nv) {
+              const uint4 v = vrow[(t0 + j) * 32];
+              const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+              for (int g = 0; g < G; ++g) {
+                const float pj = j == 0 ? p4[g].x : j == 1 ? p4[g].y : j == 2 ? p4[g].z : p4[g].w;
+                const float2 p2 = make_float2(pj, pj);
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  ov[g][e] = __ffma2_rn(p2, make_float2(__uint_as_float(w[e] << 16), __uint_as_float(w[e] & 0xffff0000u)),
+                                        ov[g][e]);
+              }
+            }
+          }
         }
       }
-      for (; t < nv; ++t) {
-        const float v = __uint_as_float((uint32_t)vcol[t * kBN] << 16);
-#pragma unroll
-        for (int g = 0; g < G; ++g) oa[g].x = fmaf(pp[g * kRows + t], v, oa[g].x);
-      }
-#pragma unroll
-      for (int g = 0; g < G; ++g) o[g] += (oa[g].x + oa[g].y) + (ob[g].x + ob[g].y);
-      bar_epi();                                       // sV / sP / sL / sRed free
+      bar_epi();                                       // sV / sP / sL / sRed / sAl free
       if (ew == 0 && lane == 0) TSTAMP(40 + it);
       if (ew == 0 && lane == 0) mbar_arrive(vempty);
+    }
+    // ---- reduce the 8 token groups' partial P V (sV is free: the V producer is done)
+    float* red = reinterpret_cast<float*>(sV);   // [8 warps][NQH][128]
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        *reinterpret_cast<float2*>(red + ((size_t)ew * NQH + kh * G + g) * kDH + 8 * (lane & 15) + 2 * e) = ov[g][e];
+    bar_epi();
+    float o[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      float acc = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) acc += red[((size_t)w * NQH + hf * G + g) * kDH + n];
+      o[g] = acc;
     }
     // ---- write y (single chunk) or the chunk's partial
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const int h = nb * NQH + hf * G + g;
-      if (a.direct_out) {
+      if (a.direct_out && gridDim.x == 1) {
         __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(a.direct_out) + ((size_t)b * a.n_q + h) * kDH;
         y[n] = __float2bfloat16_rn(l_run[g] > 0.f ? o[g] / l_run[g] : 0.f);
       } else {
@@ -496,6 +603,7 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
         if (n == 0) { dst[0] = m_run[g]; dst[1] = l_run[g]; }
       }
     }
+    if (a.counters && gridDim.x > 1) __threadfence();
   }
   tc_fence_before();
   __syncthreads();
@@ -505,6 +613,7 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
+  if (a.counters && gridDim.x > 1) merge_if_last<NQH>(a, b, nb, tid, reinterpret_cast<float*>(smem));
   pdl_launch_dependents();
 }
 
@@ -541,6 +650,11 @@ extern "C" int sals_debug_tc_trace(unsigned long long* host_out) {
   (void)host_out;
   return -1;
 #endif
+}
+
+// Largest split count the in-kernel merge can stage in shared memory.
+int tc2_merge_max_splits(int G) {
+  return (tc2::smem_bytes(G) - 1024) / (2 * G * (tc2::kDH + 3) * 4);
 }
 
 bool tc2_supported(int head_dim, int D, int rank, int G) {

@@ -23,7 +23,7 @@ STATUS = {0: "SALS_OK", 1: "SALS_ERR_INVALID_ARGUMENT", 2: "SALS_ERR_UNSUPPORTED
 EXPORTED = ["sals_workspace_bytes", "sals_append_latent", "sals_decode", "sals_decode_profile", "sals_dense_append",
             "sals_dense_workspace_bytes", "sals_dense_decode", "sals_shard_candidates", "sals_shard_attend",
             "sals_merge_partials", "sals_shard_workspace_bytes", "sals_status_string", "sals_last_error",
-            "sals_launch_count"]
+            "sals_launch_count", "sals_profile_stage_mask"]
 
 
 class SalsError(RuntimeError):
@@ -74,6 +74,7 @@ def _load():
         "sals_status_string": (ctypes.c_char_p, [I32]),
         "sals_last_error": (ctypes.c_char_p, []),
         "sals_launch_count": (ctypes.c_uint64, [I32]),
+        "sals_profile_stage_mask": (ctypes.c_uint32, [ctypes.c_uint32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -174,6 +175,14 @@ def sals_merge_partials(cfg, partial_all, world, batch, out, stream=None):
 
 def sals_launch_count(reset: bool = False) -> int:
     return int(_lib.sals_launch_count(1 if reset else 0))
+
+
+STAGE_BITS = {"qproj_rope": 0, "score": 1, "topk": 2, "recon_attn": 3, "flash": 4, "merge": 5, "append": 6}
+
+
+def sals_profile_stage_mask(mask: int) -> int:
+    """Profiling only: restrict this thread's calls to the stages in `mask` (STAGE_BITS)."""
+    return int(_lib.sals_profile_stage_mask(mask & 0xffffffff))
 
 
 def sals_status_string(status: int) -> str:
