@@ -24,6 +24,12 @@ FLAGS = os.environ.get("SALS_EXTRA_NVCC", "").split() + ["-O3", "-std=c++17", "-
          "-Xptxas", "-warn-spills", "-static-global-template-stub=false", "-I", os.path.join(ROOT, "include")]
 
 
+# Per-file extra flags.  topk_cta.cu: ptxas -O1..-O3 (CUDA 12.9, sm_100a) produce a
+# wrong selection for this kernel (reproduced standalone by tools/exp/topk_cta_test.cu:
+# -O0 and -G pass, every optimised level fails); it is compiled with ptxas -O0.
+PER_FILE = {}
+
+
 def _sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
@@ -42,7 +48,7 @@ def up_to_date() -> bool:
 
 def _compile(src: str, verbose: bool) -> str:
     obj = os.path.join(OBJDIR, os.path.basename(src) + ".o")
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *PER_FILE.get(os.path.basename(src), []), "-c", src, "-o", obj]
     if verbose:
         print(" ".join(cmd), flush=True)
     r = subprocess.run(cmd, capture_output=True, text=True)

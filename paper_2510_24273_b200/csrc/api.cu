@@ -30,6 +30,8 @@ thread_local StageTimer* g_timer = nullptr;
 // Stage mask (sals_profile_stage_mask): bit i enables stage i; bit kNumStages the append.
 thread_local uint32_t g_stage_mask = 0xffffffffu;
 // TMA score kernel for bf16 (SALS_SCORE_LSU=1 in the environment selects the LSU kernel).
+// single-CTA top-k for <= 8192 entries (SALS_TOPK_CLUSTER=1 forces the cluster kernel)
+const bool g_topk_cluster = [] { const char* e = getenv("SALS_TOPK_CLUSTER"); return e && e[0] == '1'; }();
 const bool g_fused_merge = [] { const char* e = getenv("SALS_FUSED_MERGE"); return e && e[0] == '1'; }();
 const bool g_score_tma = [] { const char* e = getenv("SALS_SCORE_LSU"); return !(e && e[0] == '1'); }();
 inline bool on(int stage) { return (g_stage_mask >> stage) & 1u; }
@@ -144,6 +146,7 @@ struct Plan {
   bool tc2;
   int tk_cs, tk_slice;     // top-k cluster size / slice
   int tk_nt, tk_cap;       // threads per CTA, candidate capacity (histogram-assisted kernel)
+  int tk_n;                // entries per request (upper bound)
   size_t tk_smem;
   int proj_cs, proj_rows;
   // workspace offsets
@@ -172,6 +175,7 @@ sals_status plan_topk(int n_entries, bool cand, Plan& p) {
   if (slice > cap) return fail(SALS_ERR_UNSUPPORTED, "top-k over %d entries exceeds the cluster limit", n_entries);
   p.tk_cs = cs;
   p.tk_slice = slice;
+  p.tk_n = n_entries;
   if (cand) {
     p.tk_nt = kTopkThreads;
     p.tk_cap = 0;
@@ -196,7 +200,8 @@ void plan_flash(int batch, int n_kv, int ntok, int tpw_unr, int& nsplit, int& ch
 int flash_tpw_unr(const sals_config* c) {
   const int epl = c->dtype == SALS_BF16 ? 8 : 4;
   const int lpt = c->head_dim / epl;
-  return (32 / lpt) * 2;
+  const int G = c->num_q_heads / c->num_kv_heads;
+  return (32 / lpt) * (G <= 2 ? 4 : 2);   // flash_decode_kernel's TPW * UNR
 }
 
 // Rows of U per CTA of the projection cluster: a multiple of 8 (16-byte vectors),
@@ -330,6 +335,10 @@ sals_status launch_topk(TopkArgs a, int batch, const Plan& p, cudaStream_t st) {
   // cluster attribute even for cs == 1 (the kernels use cluster barriers / DSMEM)
   if (a.hist0 == nullptr) {
     SALS_CUDA_TRY(launch(topk_cluster_kernel, dim3(batch * p.tk_cs), dim3(kTopkThreads), p.tk_smem, st, p.tk_cs, a));
+  } else if (a.cand_idx == nullptr && a.seg_len == 0 && p.tk_n <= 8192 && !g_topk_cluster) {
+    cudaError_t e = launch_topk_cta(a, batch, p.tk_n, st);
+    if (e != cudaSuccess) return fail(SALS_ERR_CUDA, "topk_cta launch: %s", cudaGetErrorString(e));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
   } else {
     a.cand_cap = p.tk_cap;
     if (p.tk_nt == 1024)

@@ -109,7 +109,7 @@ flash_decode_kernel(FlashArgs a) {
   constexpr int LPT = DH / EPL;            // lanes per token row
   static_assert(LPT >= 1 && LPT <= 32, "head row must fit one warp");
   constexpr int TPW = 32 / LPT;            // tokens per warp step
-  constexpr int UNR = 2;
+  constexpr int UNR = G <= 2 ? 4 : 2;   // K/V rows in flight per lane-group (register budget)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sub = lane / LPT, li = lane % LPT;
   const int b = blockIdx.z, g = blockIdx.y;
@@ -160,11 +160,13 @@ flash_decode_kernel(FlashArgs a) {
         kr[u] = vr[u] = make_uint4(0, 0, 0, 0);
       }
     }
+    // logits of the UNR tokens first, then ONE online-softmax update per head
+    // (a single max / rescale per step instead of a serial chain per token)
+    float sc[UNR][G];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      float kf[EPL], vf[EPL];
+      float kf[EPL];
       Elem<T>::unpack(kr[u], kf);
-      Elem<T>::unpack(vr[u], vf);
 #pragma unroll
       for (int h = 0; h < G; ++h) {
         float s = 0.f;
@@ -172,16 +174,29 @@ flash_decode_kernel(FlashArgs a) {
         for (int e = 0; e < EPL; ++e) s = fmaf(q[h][e], kf[e], s);
 #pragma unroll
         for (int off = LPT / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        if (ok[u]) {
-          const float mn = fmaxf(m[h], s);
-          const float corr = exp2f(m[h] - mn);      // m = -inf -> 0
-          const float p = exp2f(s - mn);
-          l[h] = l[h] * corr + p;
-#pragma unroll
-          for (int e = 0; e < EPL; ++e) o[h][e] = fmaf(p, vf[e], o[h][e] * corr);
-          m[h] = mn;
-        }
+        sc[u][h] = ok[u] ? s : -INFINITY;
       }
+    }
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      float mx = m[h];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) mx = fmaxf(mx, sc[u][h]);
+      if (mx == -INFINITY) continue;               // nothing valid yet for this lane group
+      const float corr = exp2f(m[h] - mx);         // m = -inf -> 0
+      l[h] *= corr;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) o[h][e] *= corr;
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const float p = exp2f(sc[u][h] - mx);      // -inf (invalid token) -> 0
+        float vf[EPL];
+        Elem<T>::unpack(vr[u], vf);
+        l[h] += p;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) o[h][e] = fmaf(p, vf[e], o[h][e]);
+      }
+      m[h] = mx;
     }
   }
   // merge the TPW token groups of the warp

@@ -119,6 +119,8 @@ struct OwnedArgs {        // sharded: owned selection list = owned sinks | owned
 template <typename T, bool POOL> __global__ void project_kernel(ProjectArgs a);
 template <typename T, int LG, int CPL> __global__ void latent_score_kernel(ScoreArgs a);
 // TMA-streamed bf16 scoring (score_tma.cu); cudaErrorNotSupported outside its shapes.
+// Single-CTA histogram-assisted top-k for <= 8192 entries per request (topk_cta.cu).
+cudaError_t launch_topk_cta(const TopkArgs& a, int batch, int max_entries, cudaStream_t st);
 cudaError_t launch_score_tma(const ScoreArgs& a, int batch, int max_len, cudaStream_t st, int nsm);
 __global__ void topk_cluster_kernel(TopkArgs a);
 template <int NT> __global__ void topk_hist_kernel(TopkArgs a);

@@ -254,26 +254,10 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
   const int chunk = blockIdx.x, nb = blockIdx.y, b = blockIdx.z;
   const int n0 = nb * kBN;
 
-  if (tid == 0) TSTAMP(80);
-  pdl_wait();
-  const int cnt = a.count[b];
-  const int ntiles_b = (cnt + kRows - 1) / kRows;
-  const int t_begin = chunk * a.tiles_per_cta;
-  const int t_end = min(ntiles_b, t_begin + a.tiles_per_cta);
-  const int ntile = max(0, t_end - t_begin);
-  const int* selb = a.sel + (size_t)b * a.k_stride;
-
-  if (ntile == 0) {   // no selected tokens for this chunk: empty partials (m = -inf, l = 0, o = 0)
-    for (int i = tid; i < NQH * (kDH + 2); i += kThreads) {
-      const int qh = i / (kDH + 2), j = i - qh * (kDH + 2);
-      a.partials[(((size_t)b * a.n_q + nb * NQH + qh) * a.ntiles + chunk) * (kDH + 2) + j] = j == 0 ? -INFINITY : 0.f;
-    }
-    if (a.counters) __threadfence();
-    if (a.counters) merge_if_last<NQH>(a, b, nb, tid, reinterpret_cast<float*>(smem));
-    pdl_launch_dependents();
-    return;
-  }
-
+  // Prologue before griddepcontrol.wait (overlaps the top-k kernel, which triggers
+  // its dependents early): barriers, TMEM allocation and the rotated queries
+  // (q^R comes from the query projection, which completed before the top-k's
+  // upstream did).  Only the selection (sel / count) is read after the wait.
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 128 + 1); mbar_init(&empty[s], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8); }
@@ -297,6 +281,32 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
       sQ4[i] = make_float4(qr[lo0] * sc, qr[lo1] * sc, qr[hi0] * sc, qr[hi1] * sc);
     }
   }
+  if (tid == 0) TSTAMP(80);
+  pdl_wait();
+  const int cnt = a.count[b];
+  const int ntiles_b = (cnt + kRows - 1) / kRows;
+  const int t_begin = chunk * a.tiles_per_cta;
+  const int t_end = min(ntiles_b, t_begin + a.tiles_per_cta);
+  const int ntile = max(0, t_end - t_begin);
+  const int* selb = a.sel + (size_t)b * a.k_stride;
+
+  if (ntile == 0) {   // no selected tokens for this chunk: empty partials (m = -inf, l = 0, o = 0)
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+      tc_fence_after();
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "r"(512));
+    }
+    for (int i = tid; i < NQH * (kDH + 2); i += kThreads) {
+      const int qh = i / (kDH + 2), j = i - qh * (kDH + 2);
+      a.partials[(((size_t)b * a.n_q + nb * NQH + qh) * a.ntiles + chunk) * (kDH + 2) + j] = j == 0 ? -INFINITY : 0.f;
+    }
+    if (a.counters) __threadfence();
+    if (a.counters) merge_if_last<NQH>(a, b, nb, tid, reinterpret_cast<float*>(smem));
+    pdl_launch_dependents();
+    return;
+  }
+
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -379,15 +389,19 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
     const char* latent = reinterpret_cast<const char*>(a.latent);
     const int aw = warp - 4, ch = lane & 7;
     int u = 0;
-    for (int it = 0; it < ntile; ++it) {
-      const int tile = t_begin + it;
+    // gather indices of tile it+1 are loaded while tile it's chunks are issued
+    auto load_rows = [&](int tile, int* rows) {
       const int nv = min(kRows, cnt - tile * kRows);
-      int rows[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int rl = aw * 32 + i * 4 + (lane >> 3);
         rows[i] = rl < nv ? selb[tile * kRows + rl] : -1;
       }
+    };
+    int rows[8], rows_nx[8];
+    load_rows(t_begin, rows);
+    for (int it = 0; it < ntile; ++it) {
+      if (it + 1 < ntile) load_rows(t_begin + it + 1, rows_nx);
       for (int kc = 0; kc < nk; ++kc, ++u) {
         const int s = u % kStages;
         if (u >= kStages) mbar_wait(&empty[s], ((u / kStages) - 1) & 1);
@@ -401,6 +415,8 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
         }
         cp_async_arrive_noinc(&full[s]);
       }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) rows[i] = rows_nx[i];
     }
   } else if (warp >= 8) {
     // ================= epilogue =================

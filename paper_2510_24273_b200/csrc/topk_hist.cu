@@ -148,6 +148,9 @@ topk_hist_kernel(TopkArgs a) {
 
   TKH_STAMP(0);
   pdl_wait();
+  // the reconstruction kernel may launch now: before its own wait it only sets up
+  // barriers / TMEM and stages q^R (written two kernels upstream)
+  pdl_launch_dependents();
   const int s = a.seq_len[b];
   const int n = a.n_entries ? a.n_entries[b] : s;
   const int e0 = rank * slice;
@@ -191,8 +194,11 @@ topk_hist_kernel(TopkArgs a) {
     for (int w = 0; w < NW; ++w) { const int wt = warp_tot[w]; wexcl += (w < warp) ? wt : 0; nr += wt; }
     const int incl = v + wexcl;
     int nd = all_mode0 ? 0 : a.k - x - z;                   // ranked entries still to choose
-    nd = max(0, min(nd, nr));
-    if (tid == 0) { s_digit = (nd > 0 && nd == nr) ? -1 : kH0Bins; s_need = 0; }   // all ranked / none
+    // no equality test on the clamped value (see topk_cta.cu: ptxas derived
+    // `clamp == nr` from a VIMNMX select predicate and got it wrong there)
+    const bool take_all = nd >= nr, take_none = nd <= 0;
+    nd = take_all ? nr : (take_none ? 0 : nd);
+    if (tid == 0) { s_digit = (!take_none && nr > 0 && take_all) ? -1 : kH0Bins; s_need = 0; }   // all ranked / none
     __syncthreads();
     if (nd > 0 && nd < nr) {
       int excl = incl - t;

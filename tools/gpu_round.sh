@@ -11,7 +11,7 @@ for w in c2 c3 c4; do
   timeout 600 python bench.py --workload $w --steps 20 --warmup 5 > gpurun_out/bench_${tag}_$w.json 2> gpurun_out/bench_${tag}_$w.err
   echo "bench $w rc=$?" >> $out
 done
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'project|latent_score|topk|recon|merge|flash|dense|owned' -c 400 --csv \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'project|score|topk|recon|merge|flash|dense|owned' -c 400 --csv \
   --log-file gpurun_out/launches_${tag}.csv python bench.py --workload c2 --steps 2 --warmup 3 --no-cpu-baseline --no-dense \
   > /dev/null 2>&1
 echo "ncu rc=$?" >> $out
