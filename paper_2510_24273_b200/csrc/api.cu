@@ -189,8 +189,9 @@ sals_status plan_topk(int n_entries, bool cand, Plan& p) {
 }
 
 void plan_flash(int batch, int n_kv, int ntok, int tpw_unr, int& nsplit, int& chunk) {
-  const int target = 148 * 24;
+  const int target = 148 * 48;   // warps: ~48 per SM keep enough K/V rows in flight
   int ns = std::max(1, ceil_div(target, (int64_t)batch * n_kv));
+  ns = std::min(ns, 512);   // merge_kernel's two-round-trip path holds <= 512 splits
   ns = std::min(ns, std::max(1, ceil_div(ntok, tpw_unr)));
   chunk = (int)align_up(ceil_div(ntok, ns), tpw_unr);
   chunk = std::max(chunk, tpw_unr);
@@ -201,7 +202,7 @@ int flash_tpw_unr(const sals_config* c) {
   const int epl = c->dtype == SALS_BF16 ? 8 : 4;
   const int lpt = c->head_dim / epl;
   const int G = c->num_q_heads / c->num_kv_heads;
-  return (32 / lpt) * (G <= 2 ? 4 : 2);   // flash_decode_kernel's TPW * UNR
+  return (32 / lpt) * (G <= 4 ? 4 : 2);   // flash_decode_kernel TPW * UNR
 }
 
 // Rows of U per CTA of the projection cluster: a multiple of 8 (16-byte vectors),

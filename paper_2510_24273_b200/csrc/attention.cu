@@ -109,7 +109,7 @@ flash_decode_kernel(FlashArgs a) {
   constexpr int LPT = DH / EPL;            // lanes per token row
   static_assert(LPT >= 1 && LPT <= 32, "head row must fit one warp");
   constexpr int TPW = 32 / LPT;            // tokens per warp step
-  constexpr int UNR = G <= 2 ? 4 : 2;   // K/V rows in flight per lane-group (register budget)
+  constexpr int UNR = G <= 4 ? 4 : 2;   // K/V rows in flight per lane-group (register budget)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sub = lane / LPT, li = lane % LPT;
   const int b = blockIdx.z, g = blockIdx.y;

@@ -20,7 +20,7 @@ constexpr int kProjWarps = kProjThreads / 32;
 constexpr int kProjBT = 8;        // requests per pass
 constexpr int kProjMaxRows = 512; // rows per CTA (D / CS)
 constexpr int kProjUnroll = 8;    // row loads in flight per lane
-constexpr int kProjPre = 8;       // rows per lane prefetched before griddepcontrol.wait (256 rows per CTA)
+constexpr int kProjPre = 8;       // rows per lane prefetched before griddepcontrol.wait (256 rows per CTA; 16 measured slower: 254 registers)
 
 #ifndef SALS_PROJ_MINB
 #define SALS_PROJ_MINB 1   // measured: an uncapped register budget (no spills) beats co-residence
