@@ -554,6 +554,10 @@ def main():
             build.build()
             run_sweep(args, rank, world)
         elif args.workload == "c4-sharded":
+            import torch.distributed as dist
+            if not dist.is_initialized():   # P = 1: a one-rank group (the all-gathers are copies)
+                dist.init_process_group("nccl", init_method="tcp://127.0.0.1:29511", rank=0, world_size=1,
+                                        device_id=torch.device("cuda", 0))
             from paper_2510_24273_b200 import sharded
             sharded.bench(args, rank, world)
         else:
@@ -561,8 +565,8 @@ def main():
             build.build()
             run_sals(args, rank, world)
     finally:
-        if world > 1:
-            import torch.distributed as dist
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
             dist.destroy_process_group()
 
 

@@ -426,11 +426,11 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
     // P V mapping: warp ew owns tokens [16 ew, 16 ew + 16) of every tile; lane owns
     // dims [8 (lane & 15), +8) of KV head kh = lane >> 4 (one 16-B V vector per token)
     const int kh = lane >> 4;
-    float m_run[G], l_run[G];
+    float m_run[G], l_run[G], lp[G];   // lp: this warp's share of the softmax denominator of head kh*G+g
     float2 ov[G][4];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      m_run[g] = -INFINITY; l_run[g] = 0.f;
+      m_run[g] = -INFINITY; l_run[g] = 0.f; lp[g] = 0.f;
 #pragma unroll
       for (int e = 0; e < 4; ++e) ov[g][e] = make_float2(0.f, 0.f);
     }
@@ -532,20 +532,10 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
         alpha[g] = exp2f(m_run[g] - mnew[g]);        // m_run = -inf -> 0
         const float p = (row >= 0) ? exp2f(lg[g] - mnew[g]) : 0.f;
         sP[(hf * G + g) * kPS + m] = p;
-        float v = p;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-        if (lane == 0) sRed[2 * 4 * G + (hf * 4 + rq) * G + g] = v;
-      }
-      bar_half(hf);
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const float* r = sRed + 2 * 4 * G + hf * 4 * G + g;
-        const float lt = (r[0] + r[G]) + (r[2 * G] + r[3 * G]);
-        l_run[g] = l_run[g] * alpha[g] + lt;
         m_run[g] = mnew[g];
         if (rq == 0 && lane == 0) sAl[hf * G + g] = alpha[g];
       }
+      // (the softmax denominator is summed by the P V lanes, which read every p anyway)
       bar_epi();                                       // sP / sAl of both halves visible
       mbar_wait(vfull, it & 1);
       if (ew == 0 && lane == 0) TSTAMP(32 + it);
@@ -555,6 +545,7 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           al[g] = sAl[kh * G + g];
+          lp[g] *= al[g];
 #pragma unroll
           for (int e = 0; e < 4; ++e) { ov[g][e].x *= al[g]; ov[g][e].y *= al[g]; }
         }
@@ -576,6 +567,7 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
 #pragma unroll
               for (int g = 0; g < G; ++g) {
                 const float pj = j == 0 ? p4[g].x : j == 1 ? p4[g].y : j == 2 ? p4[g].z : p4[g].w;
+                lp[g] += pj;
                 const float2 p2 = make_float2(pj, pj);
 #pragma unroll
                 for (int e = 0; e < 4; ++e)
@@ -597,7 +589,18 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
 #pragma unroll
       for (int e = 0; e < 4; ++e)
         *reinterpret_cast<float2*>(red + ((size_t)ew * NQH + kh * G + g) * kDH + 8 * (lane & 15) + 2 * e) = ov[g][e];
+    float* lred = red + 8 * NQH * kDH;           // [8 warps][NQH] denominators
+    if ((lane & 15) == 0)
+#pragma unroll
+      for (int g = 0; g < G; ++g) lred[ew * NQH + kh * G + g] = lp[g];
     bar_epi();
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      float l = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) l += lred[w * NQH + hf * G + g];
+      l_run[g] = l;
+    }
     float o[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
