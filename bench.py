@@ -2,8 +2,10 @@
 """SALS decode-attention benchmark (BASELINE.json metric) — one JSON line on rank 0.
 
 A step = decoding one token for a batch of B requests through the 32 attention
-layers of the model: per layer `sals_append_latent` (Alg. 1 lines 2-3) then
-`sals_decode` (lines 2, 4-9) on that layer's own caches.  32 distinct layers
+layers of the model: per layer `sals_append_decode` (Alg. 1 lines 2-9: the
+append of `sals_append_latent` and the whole of `sals_decode` in one call; the
+two projections share one launch) on that layer's own caches
+(`--separate-append` times the two calls instead).  32 distinct layers
 keep the per-step working set (~1.8 GB at c2) far above the 126 MB L2.  The
 step is captured once in a CUDA graph and replayed; K timed steps sit between a
 barrier + synchronize on both sides, timed with CUDA events, max over ranks.
@@ -50,6 +52,8 @@ def parse():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--path", type=int, default=0, help="0 auto, 1 SIMT, 2 tcgen05")
+    ap.add_argument("--separate-append", action="store_true",
+                    help="sals_append_latent + sals_decode per layer instead of the fused sals_append_decode")
     return ap.parse_args()
 
 
@@ -257,8 +261,12 @@ def run_sals(args, rank, world):
 
     def step():
         for l, ly in enumerate(layers):
-            sals.sals_append_latent(cfg, ly["U"], ly["k_new"], ly["v_new"], pos, ly["latent"], ly["v"])
-            sals.sals_decode(cfg, ly["U"], ly["q"], ly["latent"], ly["v"], seq, s, out[l], ws)
+            if args.separate_append:
+                sals.sals_append_latent(cfg, ly["U"], ly["k_new"], ly["v_new"], pos, ly["latent"], ly["v"])
+                sals.sals_decode(cfg, ly["U"], ly["q"], ly["latent"], ly["v"], seq, s, out[l], ws)
+            else:   # one projection launch for the append and the query (U read once)
+                sals.sals_append_decode(cfg, ly["U"], ly["k_new"], ly["v_new"], ly["q"], ly["latent"], ly["v"],
+                                        seq, s, out[l], ws)
 
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
@@ -321,6 +329,8 @@ def run_sals(args, rank, world):
         "us_per_layer_step": ms * 1e3 / L,
         "stages_us": stages_us,
         "path": "tcgen05" if stages.get("flash", 0) == 0 else "simt",
+        "api": "sals_append_latent + sals_decode" if args.separate_append else
+               "sals_append_decode (append + query projection in one launch: stage qproj_rope)",
         "roofline": roof,
         "gpu_launches": int(launches_per_step * args.steps),
         "launches_per_step": int(launches_per_step),
@@ -410,8 +420,8 @@ def run_sweep(args, rank, world):
 
                 def step():
                     for l, ly in enumerate(layers):
-                        sals.sals_append_latent(cfg, ly["U"], ly["k_new"], ly["v_new"], pos, ly["latent"], ly["v"])
-                        sals.sals_decode(cfg, ly["U"], ly["q"], ly["latent"], ly["v"], seq, n, out[l], ws)
+                        sals.sals_append_decode(cfg, ly["U"], ly["k_new"], ly["v_new"], ly["q"], ly["latent"], ly["v"],
+                                                seq, n, out[l], ws)
                 with torch.cuda.stream(stream):
                     step()
                     stream.synchronize()
@@ -483,8 +493,12 @@ def run_e2e(cfg, layers, seq, pos, s, ws, out, stream, args, world):
             dev_q.copy_(host_q, non_blocking=True)
             dev_kv.copy_(host_kv, non_blocking=True)
             for l, ly in enumerate(layers):
-                sals.sals_append_latent(cfg, ly["U"], dev_kv[l, 0], dev_kv[l, 1], pos, ly["latent"], ly["v"])
-                sals.sals_decode(cfg, ly["U"], dev_q[l], ly["latent"], ly["v"], seq, s, out[l], ws)
+                if args.separate_append:
+                    sals.sals_append_latent(cfg, ly["U"], dev_kv[l, 0], dev_kv[l, 1], pos, ly["latent"], ly["v"])
+                    sals.sals_decode(cfg, ly["U"], dev_q[l], ly["latent"], ly["v"], seq, s, out[l], ws)
+                else:
+                    sals.sals_append_decode(cfg, ly["U"], dev_kv[l, 0], dev_kv[l, 1], dev_q[l], ly["latent"], ly["v"],
+                                            seq, s, out[l], ws)
             host_out.copy_(out, non_blocking=True)
             stream.synchronize()
         for _ in range(2):

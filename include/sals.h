@@ -122,6 +122,20 @@ sals_status sals_decode(const sals_config* cfg, const void* U, const void* q,
                         void* workspace, size_t ws_bytes, void* stream);
 
 /*
+ * sals_append_decode -- sals_append_latent followed by sals_decode for the same
+ * step in ONE call (Alg. 1 lines 2-9): the new token's latent row
+ * (k~ = U^T k_new) and value row are written at slot d_seq_len[b] - 1, and the
+ * append's projection shares one launch with the query projection (U is read
+ * once for both).  Arguments as for the two calls; latent_cache and v_cache are
+ * written (row d_seq_len[b] - 1 only).  Results are identical to
+ * sals_append_latent(..., d_pos = d_seq_len - 1, ...) then sals_decode(...).
+ */
+sals_status sals_append_decode(const sals_config* cfg, const void* U, const void* k_new, const void* v_new,
+                               const void* q, void* latent_cache, void* v_cache, int64_t cap, int32_t batch,
+                               const int32_t* d_seq_len, int32_t max_seq_len, void* out, int32_t* sel_idx_out,
+                               float* scores_out, void* workspace, size_t ws_bytes, void* stream);
+
+/*
  * sals_decode_profile — profiling only: runs sals_decode `iters` times with a
  * CUDA event after every stage kernel and SYNCHRONISES the stream after each
  * run; writes the mean milliseconds of each stage to stage_ms[6] =

@@ -261,20 +261,26 @@ sals_status make_plan(const sals_config* c, int batch, int max_s, Plan& p, bool 
 }
 
 // ------------------------------------------------------------ dispatchers
+// mode 0 append, 1 query projection (+ query RoPE role), 2 both (fused append + decode)
 template <typename T>
-sals_status launch_project(const sals_config* c, const Plan& p, bool pool, ProjectArgs& a, int ncols,
-                           cudaStream_t st) {
+sals_status launch_project(const sals_config* c, const Plan& p, int mode, ProjectArgs& a, cudaStream_t st) {
   a.rows_per_cta = p.proj_rows;
-  const int ncolblk = ceil_div(ncols, 8 * (16 / (int)sizeof(T)));
-  dim3 grid(p.proj_cs, ncolblk + (pool ? 1 : 0));
+  const int cpb = 8 * (16 / (int)sizeof(T));
+  int gy;
+  if (mode == 0) gy = ceil_div(a.ncols, cpb);
+  else if (mode == 1) gy = ceil_div(a.ncols, cpb) + 1;
+  else { a.n_append_blocks = ceil_div(a.ncols_a, cpb); gy = a.n_append_blocks + ceil_div(a.ncols, cpb) + 1; }
+  dim3 grid(p.proj_cs, gy);
   static bool attr_done = false;
   if (!attr_done) {
-    SALS_CUDA_TRY(cudaFuncSetAttribute(project_kernel<T, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    SALS_CUDA_TRY(cudaFuncSetAttribute(project_kernel<T, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    SALS_CUDA_TRY(cudaFuncSetAttribute(project_kernel<T, 0>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    SALS_CUDA_TRY(cudaFuncSetAttribute(project_kernel<T, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    SALS_CUDA_TRY(cudaFuncSetAttribute(project_kernel<T, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr_done = true;
   }
-  if (pool) SALS_CUDA_TRY(launch(project_kernel<T, true>, grid, dim3(kProjThreads), 0, st, p.proj_cs, a));
-  else SALS_CUDA_TRY(launch(project_kernel<T, false>, grid, dim3(kProjThreads), 0, st, p.proj_cs, a));
+  if (mode == 0) SALS_CUDA_TRY(launch(project_kernel<T, 0>, grid, dim3(kProjThreads), 0, st, p.proj_cs, a));
+  else if (mode == 1) SALS_CUDA_TRY(launch(project_kernel<T, 1>, grid, dim3(kProjThreads), 0, st, p.proj_cs, a));
+  else SALS_CUDA_TRY(launch(project_kernel<T, 2>, grid, dim3(kProjThreads), 0, st, p.proj_cs, a));
   return SALS_OK;
 }
 
@@ -455,11 +461,13 @@ sals_status attend_list(const sals_config* c, const Plan& p, const void* U, cons
   return ms;
 }
 
+// k_new / v_new non-null: fused append + decode (sals_append_decode): one projection
+// launch writes the new latent / value rows (slot seq_len - 1) and projects the query.
 template <typename T>
 sals_status decode_impl(const sals_config* c, const void* U, const void* q, const void* latent,
                         const void* v_cache, int64_t cap, int batch, const int* seq_len, int max_s,
                         void* out, int* sel_out, float* scores_out, char* ws, const Plan& p,
-                        cudaStream_t st) {
+                        cudaStream_t st, const void* k_new = nullptr, const void* v_new = nullptr) {
   float* qtil = reinterpret_cast<float*>(ws + p.off_qtil);
   float* qrope = reinterpret_cast<float*>(ws + p.off_qrope);
   int* sel = reinterpret_cast<int*>(ws + p.off_sel);
@@ -474,7 +482,17 @@ sals_status decode_impl(const sals_config* c, const void* U, const void* q, cons
   uint32_t* hist = reinterpret_cast<uint32_t*>(ws + p.off_hist);
   pa.hist0_zero = hist; pa.hist0_words = p.hist_words;
   mark_begin(st);
-  sals_status s = on(kStQproj) ? launch_project<T>(c, p, true, pa, c->score_rank, st) : SALS_OK;
+  const bool fused = k_new != nullptr;
+  sals_status s = SALS_OK;
+  if (fused) {
+    pa.xa = k_new; pa.ncols_a = c->rank; pa.v_new = v_new; pa.pos = nullptr;
+    pa.latent = const_cast<void*>(latent); pa.v_cache = const_cast<void*>(v_cache); pa.cap = cap;
+    Plan pf = p;
+    plan_proj(pf, false);   // the append's cluster shape (more column blocks)
+    s = on(kStQproj) ? launch_project<T>(c, pf, 2, pa, st) : SALS_OK;
+  } else if (on(kStQproj)) {
+    s = launch_project<T>(c, p, 1, pa, st);
+  }
   if (s != SALS_OK) return s;
   mark(kStQproj, st);
 
@@ -482,6 +500,7 @@ sals_status decode_impl(const sals_config* c, const void* U, const void* q, cons
   sa.latent = latent; sa.cap = cap; sa.r = c->rank; sa.rstar = c->score_rank; sa.qtil = qtil;
   sa.len = seq_len; sa.scores = scores; sa.stride = sstride;
   sa.hist0 = hist; sa.seq_len = seq_len; sa.idx_base = 0; sa.sink = c->sink; sa.recent = c->recent;
+  sa.stream_after_wait = fused ? 1 : 0;   // the new latent row comes from the kernel just before
   s = on(kStScore) ? launch_score<T>(c, sa, batch, max_s, st) : SALS_OK;
   if (s != SALS_OK) return s;
   mark(kStScore, st);
@@ -551,8 +570,8 @@ sals_status sals_append_latent(const sals_config* cfg, const void* U, const void
   a.pos = d_pos; a.v_new = v_new; a.v_cache = v_cache;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (!on(kNumStages)) return SALS_OK;
-  if (cfg->dtype == SALS_BF16) return launch_project<__nv_bfloat16>(cfg, p, false, a, cfg->rank, st);
-  return launch_project<float>(cfg, p, false, a, cfg->rank, st);
+  if (cfg->dtype == SALS_BF16) return launch_project<__nv_bfloat16>(cfg, p, 0, a, st);
+  return launch_project<float>(cfg, p, 0, a, st);
 }
 
 sals_status sals_decode(const sals_config* cfg, const void* U, const void* q, const void* latent_cache,
@@ -578,6 +597,31 @@ sals_status sals_decode(const sals_config* cfg, const void* U, const void* q, co
                                       sel_idx_out, scores_out, ws, p, st);
   return decode_impl<float>(cfg, U, q, latent_cache, v_cache, cap, batch, d_seq_len, max_seq_len, out,
                             sel_idx_out, scores_out, ws, p, st);
+}
+
+sals_status sals_append_decode(const sals_config* cfg, const void* U, const void* k_new, const void* v_new,
+                               const void* q, void* latent_cache, void* v_cache, int64_t cap, int32_t batch,
+                               const int32_t* d_seq_len, int32_t max_seq_len, void* out, int32_t* sel_idx_out,
+                               float* scores_out, void* workspace, size_t ws_bytes, void* stream) {
+  sals_status s = validate(cfg);
+  if (s != SALS_OK) return s;
+  if (!U || !k_new || !v_new || !q || !latent_cache || !v_cache || !d_seq_len || !out || !workspace)
+    return fail(SALS_ERR_INVALID_ARGUMENT, "NULL tensor argument");
+  if (batch < 1 || batch > 65535) return fail(SALS_ERR_UNSUPPORTED, "batch %d outside [1, 65535]", batch);
+  if (max_seq_len < 1 || max_seq_len > cap) return fail(SALS_ERR_INVALID_ARGUMENT, "need 1 <= max_seq_len <= cap");
+  if (max_seq_len > 393216) return fail(SALS_ERR_UNSUPPORTED, "max_seq_len > 393216");
+  if (reinterpret_cast<uintptr_t>(workspace) % 256) return fail(SALS_ERR_INVALID_ARGUMENT, "workspace not 256-B aligned");
+  Plan p{};
+  s = make_plan(cfg, batch, max_seq_len, p, false);
+  if (s != SALS_OK) return s;
+  if (ws_bytes < p.total) return fail(SALS_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu", ws_bytes, p.total);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  char* ws = reinterpret_cast<char*>(workspace);
+  if (cfg->dtype == SALS_BF16)
+    return decode_impl<__nv_bfloat16>(cfg, U, q, latent_cache, v_cache, cap, batch, d_seq_len, max_seq_len, out,
+                                      sel_idx_out, scores_out, ws, p, st, k_new, v_new);
+  return decode_impl<float>(cfg, U, q, latent_cache, v_cache, cap, batch, d_seq_len, max_seq_len, out,
+                            sel_idx_out, scores_out, ws, p, st, k_new, v_new);
 }
 
 sals_status sals_decode_profile(const sals_config* cfg, const void* U, const void* q, const void* latent_cache,
@@ -669,12 +713,12 @@ sals_status sals_dense_decode(const sals_config* cfg, const void* q, const void*
   m.partials = part; m.bh_stride = (int64_t)nsplit * (cfg->head_dim + 2); m.s_stride = cfg->head_dim + 2;
   m.nsplit = nsplit; m.n_q = cfg->num_q_heads; m.head_dim = cfg->head_dim; m.out = out; m.normalize = 1;
   if (cfg->dtype == SALS_BF16) {
-    SALS_CUDA_TRY(launch(project_kernel<__nv_bfloat16, true>, dim3(1, 1), dim3(kProjThreads), 0, st, 1, pa));
+    SALS_CUDA_TRY(launch(project_kernel<__nv_bfloat16, 1>, dim3(1, 1), dim3(kProjThreads), 0, st, 1, pa));
     s = launch_flash<__nv_bfloat16, true>(cfg, f, batch, st);
     if (s != SALS_OK) return s;
     return launch_merge<__nv_bfloat16>(cfg, m, batch, st);
   }
-  SALS_CUDA_TRY(launch(project_kernel<float, true>, dim3(1, 1), dim3(kProjThreads), 0, st, 1, pa));
+  SALS_CUDA_TRY(launch(project_kernel<float, 1>, dim3(1, 1), dim3(kProjThreads), 0, st, 1, pa));
   s = launch_flash<float, true>(cfg, f, batch, st);
   if (s != SALS_OK) return s;
   return launch_merge<float>(cfg, m, batch, st);
@@ -721,10 +765,10 @@ sals_status sals_shard_candidates(const sals_config* cfg, const void* U, const v
   sa.len = d_local_len; sa.scores = scores; sa.stride = p.score_stride;
   sa.hist0 = hist; sa.seq_len = d_seq_len; sa.idx_base = shard_start; sa.sink = cfg->sink; sa.recent = cfg->recent;
   if (cfg->dtype == SALS_BF16) {
-    s = launch_project<__nv_bfloat16>(cfg, p, true, pa, cfg->score_rank, st);
+    s = launch_project<__nv_bfloat16>(cfg, p, 1, pa, st);
     if (s == SALS_OK) s = launch_score<__nv_bfloat16>(cfg, sa, batch, max_local_len, st);
   } else {
-    s = launch_project<float>(cfg, p, true, pa, cfg->score_rank, st);
+    s = launch_project<float>(cfg, p, 1, pa, st);
     if (s == SALS_OK) s = launch_score<float>(cfg, sa, batch, max_local_len, st);
   }
   if (s != SALS_OK) return s;

@@ -35,6 +35,9 @@ struct ProjectArgs {
   void* latent; int64_t cap; const int* pos;
   const void* v_new; void* v_cache;
   uint32_t* hist0_zero; int hist0_words;   // qproj: zero the score histogram (rope-role CTAs)
+  // fused append + query projection (MODE 2): append role's input / columns / block count;
+  // pos == nullptr -> the new token's slot is seq_len[b] - 1
+  const void* xa; int ncols_a; int n_append_blocks;
 };
 
 struct ScoreArgs {
@@ -49,6 +52,7 @@ struct ScoreArgs {
   const int* seq_len;   // [B] global s_b (ranked range [sink, s_b - recent))
   int64_t idx_base;     // global index of local token 0
   int sink, recent;
+  int stream_after_wait;  // 1: the latent rows may have been written by the previous kernel (fused append)
 };
 
 struct TopkArgs {
@@ -116,7 +120,7 @@ struct OwnedArgs {        // sharded: owned selection list = owned sinks | owned
   int* own_sel; int* own_count;   // [B, k] local rows, [B]
 };
 
-template <typename T, bool POOL> __global__ void project_kernel(ProjectArgs a);
+template <typename T, int MODE> __global__ void project_kernel(ProjectArgs a);
 template <typename T, int LG, int CPL> __global__ void latent_score_kernel(ScoreArgs a);
 // TMA-streamed bf16 scoring (score_tma.cu); cudaErrorNotSupported outside its shapes.
 // Single-CTA histogram-assisted top-k for <= 8192 entries per request (topk_cta.cu).

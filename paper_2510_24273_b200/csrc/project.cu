@@ -25,9 +25,16 @@ constexpr int kProjPre = 8;       // rows per lane prefetched before griddepcont
 #ifndef SALS_PROJ_MINB
 #define SALS_PROJ_MINB 1   // measured: an uncapped register budget (no spills) beats co-residence
 #endif
-template <typename T, bool POOL>
+// MODE 0: append (k~ = U^T k_new -> latent row, v row copy); 1: query projection
+// (+ query RoPE role, histogram zeroing); 2: both in one launch (sals_append_decode):
+// blockIdx.y < n_append_blocks are append column blocks, the rest the query role.
+template <typename T, int MODE>
 __global__ void __launch_bounds__(kProjThreads, SALS_PROJ_MINB)   // 2: <= 128 registers, co-resident with the next kernel
 project_kernel(ProjectArgs a) {
+  const bool pool = MODE == 1 || (MODE == 2 && (int)blockIdx.y >= a.n_append_blocks);
+  const int yb = (MODE == 2 && pool) ? (int)blockIdx.y - a.n_append_blocks : (int)blockIdx.y;   // block within the role
+  const int ncols = (MODE == 2 && !pool) ? a.ncols_a : a.ncols;
+  const int x_stride = (MODE == 2 && !pool) ? a.D : a.x_stride;
   constexpr int EPC = Elem<T>::kPer16;       // columns per lane
   constexpr int CPB = 8 * EPC;               // columns per CTA
   __shared__ float xs[kProjBT][kProjMaxRows];
@@ -38,18 +45,18 @@ project_kernel(ProjectArgs a) {
   const int rank = (int)cluster_ctarank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const T* U = reinterpret_cast<const T*>(a.U);
-  const T* x = reinterpret_cast<const T*>(a.x);
+  const T* x = reinterpret_cast<const T*>((MODE == 2 && !pool) ? a.xa : a.x);
 
   const int rows_per = a.rows_per_cta;
   const int row0 = rank * rows_per;
   const int row1 = min(a.D, row0 + rows_per);
   const int slot = lane >> 3;                       // row slot 0..3 within a warp step
   const int cl = lane & 7;                          // column vector within the CTA's block
-  const int col = blockIdx.y * CPB + cl * EPC;
-  const bool col_ok = col < a.ncols;
+  const int col = yb * CPB + cl * EPC;
+  const bool col_ok = col < ncols;
   const char* Ub = reinterpret_cast<const char*>(U);
   const size_t row_bytes = (size_t)a.r * sizeof(T);
-  const bool rope_role = POOL && blockIdx.y == gridDim.y - 1;
+  const bool rope_role = pool && blockIdx.y == gridDim.y - 1;
   // U is a weight no upstream kernel writes: issue this lane's first (for
   // D <= 16 * 256 its only) batch of U rows BEFORE waiting on the upstream
   // grid, and keep them in registers for every request pass.
@@ -111,16 +118,17 @@ project_kernel(ProjectArgs a) {
     return;
   }
 
-  if (!POOL && a.v_new != nullptr) {
+  if (!pool && a.v_new != nullptr) {
     // ---- append: copy v_new[b] -> v_cache[b, pos_b] (16-byte vectors) ----
     const int nvec = a.D * (int)sizeof(T) / 16;
-    const int ncta = CS * gridDim.y;
+    const int ncta = CS * (MODE == 2 ? a.n_append_blocks : (int)gridDim.y);
     const int cta = blockIdx.y * CS + rank;
     for (int i = cta * kProjThreads + tid; i < a.B * nvec; i += ncta * kProjThreads) {
       const int b = i / nvec, v = i % nvec;
       const uint4 val = ld_v4(reinterpret_cast<const char*>(a.v_new) + ((size_t)b * a.D) * sizeof(T) + v * 16);
+      const int pb = a.pos ? a.pos[b] : a.seq_len[b] - 1;
       *reinterpret_cast<uint4*>(reinterpret_cast<char*>(a.v_cache) +
-                                (((size_t)b * a.cap + a.pos[b]) * a.D) * sizeof(T) + v * 16) = val;
+                                (((size_t)b * a.cap + pb) * a.D) * sizeof(T) + v * 16) = val;
     }
   }
 
@@ -137,8 +145,8 @@ project_kernel(ProjectArgs a) {
 #pragma unroll
         for (int e = 0; e < EPC; ++e) v[e] = 0.f;
         if (bb < nb) {
-          const T* xb = x + (size_t)(b0 + bb) * a.x_stride;
-          if (POOL) {
+          const T* xb = x + (size_t)(b0 + bb) * x_stride;
+          if (pool) {
             const int g = c / a.head_dim, j = c - g * a.head_dim;   // EPC <= head_dim: one head per vector
             for (int hh = 0; hh < a.group; ++hh) {
               float f[EPC];
@@ -232,17 +240,18 @@ project_kernel(ProjectArgs a) {
     cluster_sync_all();
     for (int o = rank * share + tid; o < min(nout, (rank + 1) * share); o += kProjThreads) {
       const int bb = o / CPB, j = o % CPB;
-      const int cj = blockIdx.y * CPB + j;
+      const int cj = yb * CPB + j;
       const int ol = o - rank * share;
       float sum = 0.f;
       for (int c = 0; c < CS; ++c) sum += incoming[c * share + ol];
-      if (cj < a.ncols) {
+      if (cj < ncols) {
         const int b = b0 + bb;
-        if (POOL) {
-          a.out_f32[(size_t)b * a.ncols + cj] = sum;
+        if (pool) {
+          a.out_f32[(size_t)b * ncols + cj] = sum;
         } else {
           T* lat = reinterpret_cast<T*>(a.latent);
-          lat[((size_t)b * a.cap + a.pos[b]) * a.r + cj] = Elem<T>::from_f(sum);
+          const int pb = a.pos ? a.pos[b] : a.seq_len[b] - 1;
+          lat[((size_t)b * a.cap + pb) * a.r + cj] = Elem<T>::from_f(sum);
         }
       }
     }
@@ -251,9 +260,11 @@ project_kernel(ProjectArgs a) {
   pdl_launch_dependents();
 }
 
-template __global__ void project_kernel<float, false>(ProjectArgs);
-template __global__ void project_kernel<float, true>(ProjectArgs);
-template __global__ void project_kernel<__nv_bfloat16, false>(ProjectArgs);
-template __global__ void project_kernel<__nv_bfloat16, true>(ProjectArgs);
+template __global__ void project_kernel<float, 0>(ProjectArgs);
+template __global__ void project_kernel<float, 1>(ProjectArgs);
+template __global__ void project_kernel<float, 2>(ProjectArgs);
+template __global__ void project_kernel<__nv_bfloat16, 0>(ProjectArgs);
+template __global__ void project_kernel<__nv_bfloat16, 1>(ProjectArgs);
+template __global__ void project_kernel<__nv_bfloat16, 2>(ProjectArgs);
 
 }  // namespace sals

@@ -105,6 +105,7 @@ score_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant_
     // ================= producer: one TMA box per (request, 32-token chunk) =================
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(&map) : "memory");
+      if (a.stream_after_wait) pdl_wait();   // new latent rows written by the kernel just before
       int u = 0, b = i0 / nchunk, c = i0 - b * nchunk;
       int len = i0 < i1 ? a.len[b] : 0;
       for (int it = i0; it < i1; ++it) {

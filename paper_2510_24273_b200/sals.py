@@ -23,7 +23,7 @@ STATUS = {0: "SALS_OK", 1: "SALS_ERR_INVALID_ARGUMENT", 2: "SALS_ERR_UNSUPPORTED
 EXPORTED = ["sals_workspace_bytes", "sals_append_latent", "sals_decode", "sals_decode_profile", "sals_dense_append",
             "sals_dense_workspace_bytes", "sals_dense_decode", "sals_shard_candidates", "sals_shard_attend",
             "sals_merge_partials", "sals_shard_workspace_bytes", "sals_status_string", "sals_last_error",
-            "sals_launch_count", "sals_profile_stage_mask"]
+            "sals_launch_count", "sals_profile_stage_mask", "sals_append_decode"]
 
 
 class SalsError(RuntimeError):
@@ -63,6 +63,7 @@ def _load():
         "sals_workspace_bytes": (SZ, [C, I32, I32]),
         "sals_append_latent": (I32, [C, P, P, P, I32, P, P, P, I64, P]),
         "sals_decode": (I32, [C, P, P, P, P, I64, I32, P, I32, P, P, P, P, SZ, P]),
+        "sals_append_decode": (I32, [C, P, P, P, P, P, P, I64, I32, P, I32, P, P, P, P, SZ, P]),
         "sals_decode_profile": (I32, [C, P, P, P, P, I64, I32, P, I32, P, P, SZ, I32, P, P]),
         "sals_dense_append": (I32, [C, P, P, I32, P, P, P, I64, P]),
         "sals_dense_workspace_bytes": (SZ, [C, I32, I32]),
@@ -130,6 +131,15 @@ def sals_decode(cfg, U, q, latent_cache, v_cache, seq_len, max_seq_len, out, wor
 
 
 STAGES = ["qproj_rope", "score", "topk", "recon_attn", "flash", "merge"]
+
+
+def sals_append_decode(cfg, U, k_new, v_new, q, latent_cache, v_cache, seq_len, max_seq_len, out, workspace,
+                       sel_idx_out=None, scores_out=None, stream=None):
+    """sals_append_latent (slot seq_len - 1) + sals_decode in one call (one projection launch)."""
+    _check(_lib.sals_append_decode(ctypes.byref(cfg), _p(U), _p(k_new), _p(v_new), _p(q), _p(latent_cache),
+                                   _p(v_cache), latent_cache.shape[1], q.shape[0], _p(seq_len), int(max_seq_len),
+                                   _p(out), _p(sel_idx_out), _p(scores_out), _p(workspace), workspace.numel(),
+                                   _stream(stream)))
 
 
 def sals_decode_profile(cfg, U, q, latent_cache, v_cache, seq_len, max_seq_len, out, workspace, iters=10,

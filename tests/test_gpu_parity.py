@@ -261,3 +261,41 @@ def test_sharded_virtual_ranks_equal_unsharded(P, sink, recent):
     orc = O.decode(oc, host["U"], host["q"], host["latent"], host["v"], host["seq_len"], forced_selection=forced)
     H.check_output(H.widen(out), orc["y"], "bf16")
     assert np.max(np.abs(H.widen(out) - gpu["out"])) <= 2 ** -6
+
+
+# ------------------------------------------------------------------ fused append + decode
+@pytest.mark.parametrize("nkv,G,d,B,seqs", [(8, 4, 128, 3, [3000, 1777, 2048]),   # D = 1024: same clusters
+                                          (32, 1, 128, 2, [4096, 2500])])         # D = 4096
+def test_append_decode_equals_two_calls(nkv, G, d, B, seqs):
+    """sals_append_decode == sals_append_latent(slot s-1) + sals_decode: identical cache
+    rows and selection; outputs equal (D <= 2048: same projection clusters, bit-exact)
+    or within the bf16 output tolerance against the oracle on the same rows."""
+    from paper_2510_24273_b200 import sals
+    sh = dict(num_q_heads=nkv * G, num_kv_heads=nkv, head_dim=d, rank=256, score_rank=128, top_k=384,
+              rope_base=1e6, dtype="bf16")
+    cfg = sals.make_config(**sh)
+    p = synth.gen_problem(num_q_heads=nkv * G, num_kv_heads=nkv, head_dim=d, rank=256, batch=B, seq_lens=seqs, seed=11)
+    dev = lambda a: torch.from_numpy(a).cuda().bfloat16()
+    U, q, kn, vn = dev(p["U"]), dev(p["q"]), dev(p["k_new"]), dev(p["v_new"])
+    lat1, v1 = dev(p["latent"]), dev(p["v"])
+    lat2, v2 = lat1.clone(), v1.clone()
+    s_max = max(seqs)
+    seq = torch.tensor(seqs, dtype=torch.int32, device="cuda")
+    ws1 = sals.alloc_workspace(sals.sals_workspace_bytes(cfg, B, s_max), "cuda")
+    ws2 = sals.alloc_workspace(sals.sals_workspace_bytes(cfg, B, s_max), "cuda")
+    o1 = torch.empty(B, nkv * G * d, dtype=torch.bfloat16, device="cuda")
+    o2 = torch.empty_like(o1)
+    sel1 = torch.full((B, 384), -7, dtype=torch.int32, device="cuda")
+    sel2 = torch.full_like(sel1, -7)
+    sals.sals_append_latent(cfg, U, kn, vn, (seq - 1).to(torch.int32), lat1, v1)
+    sals.sals_decode(cfg, U, q, lat1, v1, seq, s_max, o1, ws1, sel_idx_out=sel1)
+    sals.sals_append_decode(cfg, U, kn, vn, q, lat2, v2, seq, s_max, o2, ws2, sel_idx_out=sel2)
+    torch.cuda.synchronize()
+    assert torch.equal(lat1, lat2) and torch.equal(v1, v2)
+    if nkv * d <= 2048:
+        assert torch.equal(sel1, sel2) and torch.equal(o1, o2)
+    else:
+        nsame = int((sel1 == sel2).all(dim=1).sum())
+        assert nsame >= B - 1
+        diff = (o1.float() - o2.float()).abs().max().item()
+        assert diff <= 2e-2, diff
