@@ -52,6 +52,10 @@ def parse():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--path", type=int, default=0, help="0 auto, 1 SIMT, 2 tcgen05")
+    ap.add_argument("--policy", choices=["alg1", "paper"], default="alg1",
+                    help="alg1: pure Algorithm 1 TopK (k = n/8); paper: the paper's serving policy (SURVEY "
+                         "§8(f) f4): sink x / recent z forced (16/64 LLaMA, 32/128 Mistral) and layers "
+                         "{0, 1, 31} dense (P:515, P:561-564)")
     ap.add_argument("--separate-append", action="store_true",
                     help="sals_append_latent + sals_decode per layer instead of the fused sals_append_decode")
     return ap.parse_args()
@@ -219,6 +223,14 @@ def run_reference(args, rank, world):
 
 
 # ------------------------------------------------------------------ GPU arm
+def policy_of(name, base, L):
+    """Selection policy of the bench step."""
+    if name == "alg1":
+        return {"name": "alg1", "sink": 0, "recent": 0, "dense_layers": ()}
+    x, z = (32, 128) if base == "c3" else (16, 64)   # (x, y, z) = 16/432/64, x2 for Mistral (P:561-564)
+    return {"name": "paper", "sink": x, "recent": z, "dense_layers": tuple(l for l in (0, 1, 31) if l < L)}
+
+
 def build_layers(sh, L, device, seed, dense):
     g = torch.Generator(device=device)
     g.manual_seed(seed)
@@ -251,17 +263,25 @@ def run_sals(args, rank, world):
     base, sh = workload_shape(args.workload)
     L, B, s = args.layers, sh["batch"], sh["seq"]
     dev = "cuda"
-    cfg = sals.make_config(**sh, path=args.path)
-    layers = build_layers(sh, L, dev, synth.SEED_BASE + 1000 * rank, dense=not args.no_dense)
+    pol = policy_of(args.policy, base, L)
+    cfg = sals.make_config(**sh, path=args.path, sink=pol["sink"], recent=pol["recent"])
+    layers = build_layers(sh, L, dev, synth.SEED_BASE + 1000 * rank,
+                          dense=(not args.no_dense) or bool(pol["dense_layers"]))
     D, nqd = sh["num_kv_heads"] * sh["head_dim"], sh["num_q_heads"] * sh["head_dim"]
     seq = torch.full((B,), s, dtype=torch.int32, device=dev)
     pos = seq - 1
     ws = sals.alloc_workspace(sals.sals_workspace_bytes(cfg, B, s), dev)
+    wsd_pol = sals.alloc_workspace(sals.sals_dense_workspace_bytes(cfg, B, s), dev) if pol["dense_layers"] else None
     out = torch.empty(L, B, nqd, dtype=torch.bfloat16, device=dev)
 
-    def step():
+    def step(sals_only=False):
         for l, ly in enumerate(layers):
-            if args.separate_append:
+            if l in pol["dense_layers"]:   # the paper keeps these layers dense
+                if sals_only:
+                    continue
+                sals.sals_dense_append(cfg, ly["k_new"], ly["v_new"], pos, ly["k_dense"], ly["v"])
+                sals.sals_dense_decode(cfg, ly["q"], ly["k_dense"], ly["v"], seq, s, out[l], wsd_pol)
+            elif args.separate_append:
                 sals.sals_append_latent(cfg, ly["U"], ly["k_new"], ly["v_new"], pos, ly["latent"], ly["v"])
                 sals.sals_decode(cfg, ly["U"], ly["q"], ly["latent"], ly["v"], seq, s, out[l], ws)
             else:   # one projection launch for the append and the query (U read once)
@@ -287,7 +307,8 @@ def run_sals(args, rank, world):
     # launching stream and timed with CUDA events; ms per launch = graph time / layers.
     # Inputs are what the full step left in the workspace.  Back-to-back launches of one
     # kernel overlap prologue/epilogue through PDL exactly as in the full step.
-    stages = stage_times(sals, step, stream, args, world, L)
+    n_sals_layers = L - len(pol["dense_layers"])
+    stages = stage_times(sals, lambda: step(True), stream, args, world, n_sals_layers)
     stages_us = {k: round(v * 1e3, 2) for k, v in stages.items() if v > 0}
 
     # ---- dense comparator (same build), same batch / layers
@@ -314,7 +335,7 @@ def run_sals(args, rank, world):
                  "kernel": "in-build split-K flash decode over the full post-RoPE K/V cache"}
 
     # ---- e2e through the public API with host buffers
-    e2e = run_e2e(cfg, layers, seq, pos, s, ws, out, stream, args, world)
+    e2e = run_e2e(cfg, layers, seq, pos, s, ws, out, stream, args, world, pol, wsd_pol)
 
     # ---- roofline of the dominant kernel
     peaks, peak_kind = load_peaks()
@@ -329,6 +350,7 @@ def run_sals(args, rank, world):
         "us_per_layer_step": ms * 1e3 / L,
         "stages_us": stages_us,
         "path": "tcgen05" if stages.get("flash", 0) == 0 else "simt",
+        "policy": {k: (list(v) if isinstance(v, tuple) else v) for k, v in pol.items()},
         "api": "sals_append_latent + sals_decode" if args.separate_append else
                "sals_append_decode (append + query projection in one launch: stage qproj_rope)",
         "roofline": roof,
@@ -477,7 +499,7 @@ def run_sweep(args, rank, world):
         print(json.dumps(line), flush=True)
 
 
-def run_e2e(cfg, layers, seq, pos, s, ws, out, stream, args, world):
+def run_e2e(cfg, layers, seq, pos, s, ws, out, stream, args, world, pol=None, wsd_pol=None):
     from paper_2510_24273_b200 import sals
     L = len(layers)
     B = seq.shape[0]
@@ -493,7 +515,10 @@ def run_e2e(cfg, layers, seq, pos, s, ws, out, stream, args, world):
             dev_q.copy_(host_q, non_blocking=True)
             dev_kv.copy_(host_kv, non_blocking=True)
             for l, ly in enumerate(layers):
-                if args.separate_append:
+                if pol and l in pol["dense_layers"]:
+                    sals.sals_dense_append(cfg, dev_kv[l, 0], dev_kv[l, 1], pos, ly["k_dense"], ly["v"])
+                    sals.sals_dense_decode(cfg, dev_q[l], ly["k_dense"], ly["v"], seq, s, out[l], wsd_pol)
+                elif args.separate_append:
                     sals.sals_append_latent(cfg, ly["U"], dev_kv[l, 0], dev_kv[l, 1], pos, ly["latent"], ly["v"])
                     sals.sals_decode(cfg, ly["U"], dev_q[l], ly["latent"], ly["v"], seq, s, out[l], ws)
                 else:

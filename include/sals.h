@@ -122,6 +122,21 @@ sals_status sals_decode(const sals_config* cfg, const void* U, const void* q,
                         void* workspace, size_t ws_bytes, void* stream);
 
 /*
+ * sals_append_latent_bulk -- prefill: Eq. 1 / Alg. 1 line 3
+ * for n_tokens consecutive tokens of every request at once:
+ *   latent_cache[b, start + i, :] = U^T k[b, i, :],  v_cache[b, start + i, :] = v[b, i, :]
+ *   k, v    [B, n_tokens, D]  PRE-RoPE keys / values (device)
+ *   start   host: slot of token 0 (the same for every request), start + n_tokens <= cap
+ * A plain dense GEMM (no fused epilogue): cuBLAS (bf16 in, fp32 accumulate,
+ * rounded to dtype), written straight into the cache rows.  Uses a cuBLAS
+ * handle created on the calling thread's first call (the only state the
+ * library keeps besides the comm handle).  Not CUDA-graph captured by the tests.
+ */
+sals_status sals_append_latent_bulk(const sals_config* cfg, const void* U, const void* k, const void* v,
+                                    int32_t batch, int32_t n_tokens, int64_t start, void* latent_cache,
+                                    void* v_cache, int64_t cap, void* stream);
+
+/*
  * sals_append_decode -- sals_append_latent followed by sals_decode for the same
  * step in ONE call (Alg. 1 lines 2-9): the new token's latent row
  * (k~ = U^T k_new) and value row are written at slot d_seq_len[b] - 1, and the

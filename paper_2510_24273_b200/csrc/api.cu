@@ -599,6 +599,23 @@ sals_status sals_decode(const sals_config* cfg, const void* U, const void* q, co
                             sel_idx_out, scores_out, ws, p, st);
 }
 
+int sals_prefill_impl(const sals_config* cfg, const void* U, const void* k, const void* v, int32_t batch,
+                      int32_t n_tokens, int64_t start, void* latent_cache, void* v_cache, int64_t cap, void* stream);
+const char* sals_prefill_last_error(void);
+
+sals_status sals_append_latent_bulk(const sals_config* cfg, const void* U, const void* k, const void* v,
+                                    int32_t batch, int32_t n_tokens, int64_t start, void* latent_cache,
+                                    void* v_cache, int64_t cap, void* stream) {
+  sals_status s = validate(cfg);
+  if (s != SALS_OK) return s;
+  if (!U || !k || !v || !latent_cache || !v_cache) return fail(SALS_ERR_INVALID_ARGUMENT, "NULL tensor argument");
+  if (batch < 1 || n_tokens < 1 || cap < 1 || start < 0 || start + n_tokens > cap)
+    return fail(SALS_ERR_INVALID_ARGUMENT, "need batch, n_tokens >= 1 and 0 <= start, start + n_tokens <= cap");
+  if (sals_prefill_impl(cfg, U, k, v, batch, n_tokens, start, latent_cache, v_cache, cap, stream) != 0)
+    return fail(SALS_ERR_CUDA, "%s", sals_prefill_last_error());
+  return SALS_OK;
+}
+
 sals_status sals_append_decode(const sals_config* cfg, const void* U, const void* k_new, const void* v_new,
                                const void* q, void* latent_cache, void* v_cache, int64_t cap, int32_t batch,
                                const int32_t* d_seq_len, int32_t max_seq_len, void* out, int32_t* sel_idx_out,

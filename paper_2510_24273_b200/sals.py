@@ -23,7 +23,8 @@ STATUS = {0: "SALS_OK", 1: "SALS_ERR_INVALID_ARGUMENT", 2: "SALS_ERR_UNSUPPORTED
 EXPORTED = ["sals_workspace_bytes", "sals_append_latent", "sals_decode", "sals_decode_profile", "sals_dense_append",
             "sals_dense_workspace_bytes", "sals_dense_decode", "sals_shard_candidates", "sals_shard_attend",
             "sals_merge_partials", "sals_shard_workspace_bytes", "sals_status_string", "sals_last_error",
-            "sals_launch_count", "sals_profile_stage_mask", "sals_append_decode"]
+            "sals_launch_count", "sals_profile_stage_mask", "sals_append_decode",
+            "sals_append_latent_bulk"]
 
 
 class SalsError(RuntimeError):
@@ -64,6 +65,7 @@ def _load():
         "sals_append_latent": (I32, [C, P, P, P, I32, P, P, P, I64, P]),
         "sals_decode": (I32, [C, P, P, P, P, I64, I32, P, I32, P, P, P, P, SZ, P]),
         "sals_append_decode": (I32, [C, P, P, P, P, P, P, I64, I32, P, I32, P, P, P, P, SZ, P]),
+        "sals_append_latent_bulk": (I32, [C, P, P, P, I32, I32, I64, P, P, I64, P]),
         "sals_decode_profile": (I32, [C, P, P, P, P, I64, I32, P, I32, P, P, SZ, I32, P, P]),
         "sals_dense_append": (I32, [C, P, P, I32, P, P, P, I64, P]),
         "sals_dense_workspace_bytes": (SZ, [C, I32, I32]),
@@ -131,6 +133,12 @@ def sals_decode(cfg, U, q, latent_cache, v_cache, seq_len, max_seq_len, out, wor
 
 
 STAGES = ["qproj_rope", "score", "topk", "recon_attn", "flash", "merge"]
+
+
+def sals_append_latent_bulk(cfg, U, k, v, start, latent_cache, v_cache, stream=None):
+    """Prefill: latent/value rows [start, start + n) of every request from k, v [B, n, D]."""
+    _check(_lib.sals_append_latent_bulk(ctypes.byref(cfg), _p(U), _p(k), _p(v), k.shape[0], k.shape[1], int(start),
+                                        _p(latent_cache), _p(v_cache), latent_cache.shape[1], _stream(stream)))
 
 
 def sals_append_decode(cfg, U, k_new, v_new, q, latent_cache, v_cache, seq_len, max_seq_len, out, workspace,

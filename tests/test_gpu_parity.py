@@ -299,3 +299,33 @@ def test_append_decode_equals_two_calls(nkv, G, d, B, seqs):
         assert nsame >= B - 1
         diff = (o1.float() - o2.float()).abs().max().item()
         assert diff <= 2e-2, diff
+
+
+# ------------------------------------------------------------------ prefill (bulk append)
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_append_latent_bulk(dtype):
+    """Prefill rows [start, start + n) == U^T k (fp64 oracle, one rounding of the stored
+    type), value rows copied; rows outside the block untouched; a decode after a bulk
+    prefill equals the oracle as usual."""
+    from paper_2510_24273_b200 import sals
+    nkv, G, d, r, B, n, start, cap = 4, 2, 64, 128, 3, 300, 17, 400
+    sh = dict(num_q_heads=nkv * G, num_kv_heads=nkv, head_dim=d, rank=r, score_rank=64, top_k=96, rope_base=1e4,
+              dtype=dtype)
+    cfg = sals.make_config(**sh)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    rng = np.random.default_rng(5)
+    D = nkv * d
+    U = torch.from_numpy(synth.orthonormal(rng, D, r)).cuda().to(tdt)
+    k = torch.from_numpy(rng.normal(size=(B, n, D))).cuda().to(tdt)
+    v = torch.from_numpy(rng.normal(size=(B, n, D))).cuda().to(tdt)
+    lat = torch.full((B, cap, r), 7.0, dtype=tdt, device="cuda")
+    vc = torch.full((B, cap, D), 7.0, dtype=tdt, device="cuda")
+    sals.sals_append_latent_bulk(cfg, U, k, v, start, lat, vc)
+    torch.cuda.synchronize()
+    ref = O.project_latent(H.widen(U), H.widen(k).reshape(B * n, D)).reshape(B, n, r)
+    got = H.widen(lat[:, start:start + n])
+    tol = (2.0 ** -7 if dtype == "bf16" else 1e-5) * np.abs(ref) + 1e-3 * (1 if dtype == "bf16" else 1e-2)
+    assert np.all(np.abs(got - ref) <= tol), np.max(np.abs(got - ref))
+    assert torch.equal(vc[:, start:start + n], v)
+    assert bool((lat[:, :start] == 7.0).all()) and bool((lat[:, start + n:] == 7.0).all())
+    assert bool((vc[:, :start] == 7.0).all()) and bool((vc[:, start + n:] == 7.0).all())
