@@ -19,7 +19,7 @@ int main(int argc, char** argv) {
   srand(1);
   for (int trial = 0; trial < 40; ++trial) {
     const int B = 1 + trial % 3;
-    const int n = 32 + rand() % 8000;
+    const int n = (trial < 30) ? 32 + rand() % 8000 : 8192 + rand() % 120000;
     const int k = 1 + rand() % n;
     const int stride = (n + 3) / 4 * 4;
     std::vector<float> sc(B * stride, 0.f);
