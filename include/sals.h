@@ -137,6 +137,24 @@ sals_status sals_append_latent_bulk(const sals_config* cfg, const void* U, const
                                     void* v_cache, int64_t cap, void* stream);
 
 /*
+ * sals_calibrate -- offline calibration of the latent basis (
+ * Sec. 4.2): C = K^T K over the stacked pre-RoPE calibration keys,
+ * C = U S U^T, U_r = the leading r = cfg->rank eigenvectors.
+ *   K            [n_rows, D] device, dtype (heads merged: D = n_kv * d)
+ *   U_out        [D, r] device, dtype: columns in descending eigenvalue order
+ *                (so the first r* columns span the score subspace), each column
+ *                signed so that its largest-magnitude component is positive
+ *   eigvals_out  [D] fp32 device or NULL: eigenvalues of C, descending
+ *   workspace    >= sals_calibrate_workspace_bytes(cfg) bytes (D^2 fp32 + solver)
+ * Gram matrix on cuBLAS (fp32 accumulate), eigensolver cuSOLVER syevd (fp32);
+ * library-owned cuBLAS / cuSOLVER handles per calling thread.  Synchronises
+ * internally (cuSOLVER); not for the decode hot path.
+ */
+size_t sals_calibrate_workspace_bytes(const sals_config* cfg);
+sals_status sals_calibrate(const sals_config* cfg, const void* K, int64_t n_rows, void* U_out, float* eigvals_out,
+                           void* workspace, size_t ws_bytes, void* stream);
+
+/*
  * sals_append_decode -- sals_append_latent followed by sals_decode for the same
  * step in ONE call (Alg. 1 lines 2-9): the new token's latent row
  * (k~ = U^T k_new) and value row are written at slot d_seq_len[b] - 1, and the

@@ -319,3 +319,31 @@ def lse_merge(ms: np.ndarray, ls: np.ndarray, os_: np.ndarray) -> np.ndarray:
     w = np.where(np.isneginf(ms), 0.0, np.exp(ms - M))
     L = (w * ls).sum(axis=0)
     return (w[..., None] * os_).sum(axis=0) / L[:, None]
+
+
+# ------------------------------------------------------------------ calibration
+def calibrate(K: np.ndarray, r: int):
+    """Offline calibration (Sec. 4.2): C = K^T K over the stacked
+    pre-RoPE keys K [N, nd] (heads merged); C = U S U^T; U_r = the leading
+    r eigenvectors.  Returns (U_r [nd, r] with columns in descending eigenvalue
+    order, all eigenvalues descending).  Library primitive: ``np.linalg.eigh``.
+    Eigenvectors are defined up to sign; each column is signed so that its
+    largest-magnitude component is positive (first such index on ties) -- a
+    convention of this build, not of the paper."""
+    K = np.asarray(K, dtype=np.float64)
+    C = K.T @ K
+    w, V = np.linalg.eigh(C)                 # ascending
+    order = np.argsort(-w, kind="stable")
+    w, V = w[order], V[:, order]
+    U = V[:, :r].copy()
+    for j in range(r):
+        i = int(np.argmax(np.abs(U[:, j])))
+        if U[i, j] < 0:
+            U[:, j] = -U[:, j]
+    return U, w
+
+
+def captured_variance(U: np.ndarray, K: np.ndarray) -> float:
+    """E(U) = ||K U||_F^2 = tr(U^T K^T K U): the key energy kept by the projection (Lemma 1)."""
+    KU = np.asarray(K, dtype=np.float64) @ np.asarray(U, dtype=np.float64)
+    return float(np.sum(KU * KU))

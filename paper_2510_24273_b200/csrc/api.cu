@@ -603,6 +603,27 @@ int sals_prefill_impl(const sals_config* cfg, const void* U, const void* k, cons
                       int32_t n_tokens, int64_t start, void* latent_cache, void* v_cache, int64_t cap, void* stream);
 const char* sals_prefill_last_error(void);
 
+size_t sals_calibrate_ws_impl(int D);
+int sals_calibrate_impl(const sals_config* cfg, const void* K, int64_t n_rows, void* U_out, float* eig_out,
+                        void* workspace, size_t ws_bytes, void* stream);
+
+size_t sals_calibrate_workspace_bytes(const sals_config* cfg) {
+  if (validate(cfg) != SALS_OK) return 0;
+  return sals_calibrate_ws_impl(cfg->num_kv_heads * cfg->head_dim);
+}
+
+sals_status sals_calibrate(const sals_config* cfg, const void* K, int64_t n_rows, void* U_out, float* eigvals_out,
+                           void* workspace, size_t ws_bytes, void* stream) {
+  sals_status s = validate(cfg);
+  if (s != SALS_OK) return s;
+  if (!K || !U_out || !workspace) return fail(SALS_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (n_rows < 1 || n_rows > 0x7fffffff) return fail(SALS_ERR_INVALID_ARGUMENT, "n_rows out of range");
+  const int rc = sals_calibrate_impl(cfg, K, n_rows, U_out, eigvals_out, workspace, ws_bytes, stream);
+  if (rc == 3) return fail(SALS_ERR_WORKSPACE_TOO_SMALL, "%s", sals_prefill_last_error());
+  if (rc != 0) return fail(SALS_ERR_CUDA, "%s", sals_prefill_last_error());
+  return SALS_OK;
+}
+
 sals_status sals_append_latent_bulk(const sals_config* cfg, const void* U, const void* k, const void* v,
                                     int32_t batch, int32_t n_tokens, int64_t start, void* latent_cache,
                                     void* v_cache, int64_t cap, void* stream) {

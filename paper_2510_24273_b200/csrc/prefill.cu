@@ -60,3 +60,116 @@ extern "C" int sals_prefill_impl(const sals_config* cfg, const void* U, const vo
   }
   return 0;
 }
+
+// ---------------------------------------------------------------------------
+// Offline calibration (§4.2): C = K^T K over the
+// stacked pre-RoPE calibration keys K [N, D], eigen-decomposition C = U S U^T,
+// U_r = the leading r eigenvectors (descending eigenvalue order, which is what
+// makes the first r* columns the score subspace).  Library primitives: the
+// Gram matrix on cuBLAS (fp32 accumulate), the symmetric eigensolver on
+// cuSOLVER (syevd, fp32); one kernel reorders / sign-normalises the columns
+// (the largest-magnitude component of each column is made positive, first such
+// index on ties) and converts to the storage type.
+#include <cusolverDn.h>
+#include <cuda_bf16.h>
+
+namespace {
+thread_local cusolverDnHandle_t g_cusolver = nullptr;
+
+__global__ void calib_columns_kernel(const float* __restrict__ evec, const float* __restrict__ w, int D, int r,
+                                     void* U_out, int bf16, float* eig_out) {
+  const int j = blockIdx.x;                 // output column: eigenvector of the j-th largest eigenvalue
+  const float* col = evec + (size_t)(D - 1 - j) * D;
+  __shared__ float s_v[32];
+  __shared__ int s_i[32];
+  float best = -1.f;
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x; i < D; i += blockDim.x) {
+    const float a = fabsf(col[i]);
+    if (a > best || (a == best && i < bi)) { best = a; bi = i; }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) { s_v[warp] = best; s_i[warp] = bi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k)
+      if (s_v[k] > s_v[0] || (s_v[k] == s_v[0] && s_i[k] < s_i[0])) { s_v[0] = s_v[k]; s_i[0] = s_i[k]; }
+  }
+  if (eig_out)   // all D eigenvalues, descending (block j writes j, j + r, ...)
+    for (int i = j + (int)threadIdx.x * (int)gridDim.x; i < D; i += (int)(blockDim.x * gridDim.x)) eig_out[i] = w[D - 1 - i];
+  __syncthreads();
+  const float sgn = col[s_i[0]] < 0.f ? -1.f : 1.f;
+  for (int i = threadIdx.x; i < D; i += blockDim.x) {
+    const float v = sgn * col[i];
+    if (bf16) reinterpret_cast<__nv_bfloat16*>(U_out)[(size_t)i * r + j] = __float2bfloat16_rn(v);
+    else reinterpret_cast<float*>(U_out)[(size_t)i * r + j] = v;
+  }
+}
+
+bool calib_handles(cudaStream_t st) {
+  if (!g_cublas && cublasCreate(&g_cublas) != CUBLAS_STATUS_SUCCESS) { g_prefill_err = "cublasCreate failed"; return false; }
+  if (!g_cusolver && cusolverDnCreate(&g_cusolver) != CUSOLVER_STATUS_SUCCESS) {
+    g_prefill_err = "cusolverDnCreate failed";
+    return false;
+  }
+  cublasSetStream(g_cublas, st);
+  cusolverDnSetStream(g_cusolver, st);
+  return true;
+}
+
+size_t align256(size_t v) { return (v + 255) / 256 * 256; }
+}  // namespace
+
+extern "C" size_t sals_calibrate_ws_impl(int D) {
+  if (!calib_handles(0)) return 0;
+  int lwork = 0;
+  if (cusolverDnSsyevd_bufferSize(g_cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, D, nullptr, D,
+                                  nullptr, &lwork) != CUSOLVER_STATUS_SUCCESS)
+    return 0;
+  return align256((size_t)D * D * 4) + align256((size_t)D * 4) + align256(4) + align256((size_t)lwork * 4);
+}
+
+extern "C" int sals_calibrate_impl(const sals_config* cfg, const void* K, int64_t n_rows, void* U_out,
+                                   float* eig_out, void* workspace, size_t ws_bytes, void* stream) {
+  const int D = cfg->num_kv_heads * cfg->head_dim, r = cfg->rank;
+  const bool bf16 = cfg->dtype == SALS_BF16;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (!calib_handles(st)) return 1;
+  int lwork = 0;
+  if (cusolverDnSsyevd_bufferSize(g_cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, D, nullptr, D,
+                                  nullptr, &lwork) != CUSOLVER_STATUS_SUCCESS) {
+    g_prefill_err = "syevd buffer size query failed";
+    return 1;
+  }
+  char* ws = reinterpret_cast<char*>(workspace);
+  float* C = reinterpret_cast<float*>(ws);
+  float* W = reinterpret_cast<float*>(ws + align256((size_t)D * D * 4));
+  int* info = reinterpret_cast<int*>(ws + align256((size_t)D * D * 4) + align256((size_t)D * 4));
+  float* work = reinterpret_cast<float*>(ws + align256((size_t)D * D * 4) + align256((size_t)D * 4) + align256(4));
+  if (ws_bytes < align256((size_t)D * D * 4) + align256((size_t)D * 4) + align256(4) + align256((size_t)lwork * 4)) {
+    g_prefill_err = "calibration workspace too small";
+    return 3;
+  }
+  // C (col-major D x D) = K_cm (D x N, ld D) * K_cm^T
+  const float one = 1.f, zero = 0.f;
+  const cudaDataType_t t = bf16 ? CUDA_R_16BF : CUDA_R_32F;
+  if (cublasGemmEx(g_cublas, CUBLAS_OP_N, CUBLAS_OP_T, D, D, (int)n_rows, &one, K, t, D, K, t, D, &zero, C,
+                   CUDA_R_32F, D, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS) {
+    g_prefill_err = "Gram matrix GEMM failed";
+    return 1;
+  }
+  if (cusolverDnSsyevd(g_cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, D, C, D, W, work, lwork,
+                       info) != CUSOLVER_STATUS_SUCCESS) {
+    g_prefill_err = "syevd failed";
+    return 1;
+  }
+  calib_columns_kernel<<<r, 256, 0, st>>>(C, W, D, r, U_out, bf16 ? 1 : 0, eig_out);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { g_prefill_err = cudaGetErrorString(e); return 1; }
+  return 0;
+}

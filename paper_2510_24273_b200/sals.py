@@ -24,7 +24,7 @@ EXPORTED = ["sals_workspace_bytes", "sals_append_latent", "sals_decode", "sals_d
             "sals_dense_workspace_bytes", "sals_dense_decode", "sals_shard_candidates", "sals_shard_attend",
             "sals_merge_partials", "sals_shard_workspace_bytes", "sals_status_string", "sals_last_error",
             "sals_launch_count", "sals_profile_stage_mask", "sals_append_decode",
-            "sals_append_latent_bulk"]
+            "sals_append_latent_bulk", "sals_calibrate_workspace_bytes", "sals_calibrate"]
 
 
 class SalsError(RuntimeError):
@@ -66,6 +66,8 @@ def _load():
         "sals_decode": (I32, [C, P, P, P, P, I64, I32, P, I32, P, P, P, P, SZ, P]),
         "sals_append_decode": (I32, [C, P, P, P, P, P, P, I64, I32, P, I32, P, P, P, P, SZ, P]),
         "sals_append_latent_bulk": (I32, [C, P, P, P, I32, I32, I64, P, P, I64, P]),
+        "sals_calibrate_workspace_bytes": (SZ, [C]),
+        "sals_calibrate": (I32, [C, P, I64, P, P, P, SZ, P]),
         "sals_decode_profile": (I32, [C, P, P, P, P, I64, I32, P, I32, P, P, SZ, I32, P, P]),
         "sals_dense_append": (I32, [C, P, P, I32, P, P, P, I64, P]),
         "sals_dense_workspace_bytes": (SZ, [C, I32, I32]),
@@ -133,6 +135,17 @@ def sals_decode(cfg, U, q, latent_cache, v_cache, seq_len, max_seq_len, out, wor
 
 
 STAGES = ["qproj_rope", "score", "topk", "recon_attn", "flash", "merge"]
+
+
+def sals_calibrate_workspace_bytes(cfg) -> int:
+    return int(_lib.sals_calibrate_workspace_bytes(ctypes.byref(cfg)))
+
+
+def sals_calibrate(cfg, K, U_out, eigvals_out=None, stream=None):
+    """Offline calibration: U_out [D, r] = leading eigenvectors of K^T K (K [N, D] pre-RoPE keys)."""
+    ws = alloc_workspace(sals_calibrate_workspace_bytes(cfg), K.device)
+    _check(_lib.sals_calibrate(ctypes.byref(cfg), _p(K), K.shape[0], _p(U_out), _p(eigvals_out), _p(ws),
+                               ws.numel(), _stream(stream)))
 
 
 def sals_append_latent_bulk(cfg, U, k, v, start, latent_cache, v_cache, stream=None):

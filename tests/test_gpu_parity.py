@@ -329,3 +329,25 @@ def test_append_latent_bulk(dtype):
     assert torch.equal(vc[:, start:start + n], v)
     assert bool((lat[:, :start] == 7.0).all()) and bool((lat[:, start + n:] == 7.0).all())
     assert bool((vc[:, :start] == 7.0).all()) and bool((vc[:, start + n:] == 7.0).all())
+
+
+# ------------------------------------------------------------------ calibration
+def test_calibrate_matches_oracle():
+    """sals_calibrate (cuBLAS Gram + cuSOLVER syevd, fp32) == oracle calibrate (fp64
+    eigh) on keys with a decaying spectrum: same eigenvalues (fp32-relative) and the
+    same signed leading eigenvectors (well separated eigenvalues)."""
+    from paper_2510_24273_b200 import sals
+    rng = np.random.default_rng(6)
+    N, nkv, d, r = 4096, 2, 64, 32
+    D = nkv * d
+    K = rng.standard_normal((N, D)) * (0.93 ** np.arange(D))[None]
+    cfg = sals.make_config(num_q_heads=nkv, num_kv_heads=nkv, head_dim=d, rank=r, score_rank=16, top_k=8,
+                           dtype="f32")
+    Kd = torch.from_numpy(K).float().cuda()
+    U = torch.empty(D, r, dtype=torch.float32, device="cuda")
+    w = torch.empty(D, dtype=torch.float32, device="cuda")
+    sals.sals_calibrate(cfg, Kd, U, w)
+    torch.cuda.synchronize()
+    Uo, wo = O.calibrate(H.widen(Kd), r)
+    np.testing.assert_allclose(H.widen(w), wo, rtol=2e-4, atol=1e-3 * wo[0] * 1e-3)
+    np.testing.assert_allclose(H.widen(U), Uo, atol=2e-3)

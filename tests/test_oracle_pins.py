@@ -339,3 +339,57 @@ def test_memory_model_matches_paper_table2_and_p427():
         ratio = traffic.sals_access_ratio(c["d_r"] * c["r_star_over_r"], c["d_r"], c["k_s"])
         assert abs(ratio - c["table2_access"]) <= c["abs_tol"]
         assert abs(1.0 / c["table2_access"] - c["p427_reduction"]) < 0.01
+
+
+# ------------------------------------------------------------------ calibration (Sec. 4.2, Lemma 1)
+def test_calibrate_eigenpairs_and_ky_fan():
+    """U_r from calibrate() satisfies C U = U diag(w_:r) (the eigen-equation, not a
+    re-call of eigh), is column-orthonormal, and captures tr(U^T C U) = sum of the
+    r largest eigenvalues -- the Ky Fan maximum, which no other orthonormal U beats."""
+    rng = np.random.default_rng(3)
+    N, D, r = 600, 24, 6
+    K = rng.standard_normal((N, D)) * (0.7 ** np.arange(D))
+    U, w = O.calibrate(K, r)
+    C = K.T @ K
+    np.testing.assert_allclose(C @ U, U * w[:r], atol=1e-8 * w[0])
+    np.testing.assert_allclose(U.T @ U, np.eye(r), atol=1e-12)
+    assert np.all(np.diff(w) <= 1e-12)
+    E = O.captured_variance(U, K)
+    np.testing.assert_allclose(E, w[:r].sum(), rtol=1e-12)
+    for _ in range(20):
+        Q, _ = np.linalg.qr(rng.standard_normal((D, r)))
+        assert O.captured_variance(Q, K) <= E * (1 + 1e-12)
+    # sign convention: the largest-magnitude component of every column is positive
+    assert all(U[int(np.argmax(np.abs(U[:, j]))), j] > 0 for j in range(r))
+
+
+def test_calibrate_recovers_a_planted_subspace():
+    """Keys that live in an r-dimensional subspace are reconstructed exactly by
+    U_r U_r^T (projection error 0: the discarded eigenvalues are 0)."""
+    rng = np.random.default_rng(4)
+    D, r = 20, 5
+    B, _ = np.linalg.qr(rng.standard_normal((D, r)))
+    K = rng.standard_normal((300, r)) @ B.T
+    U, w = O.calibrate(K, r)
+    np.testing.assert_allclose(K @ U @ U.T, K, atol=1e-10)
+    assert np.all(np.abs(w[r:]) < 1e-9 * w[0])
+
+
+def test_lemma1_joint_projection_captures_at_least_per_head():
+    """Lemma 1: the best joint multi-head projection (rank r over nd)
+    keeps at least the energy of the best per-head block-diagonal projection
+    (rank r/n per head), for correlated heads strictly more."""
+    rng = np.random.default_rng(5)
+    n, d, r = 4, 8, 8
+    base = rng.standard_normal((500, 3))
+    K = np.concatenate([base @ rng.standard_normal((3, d)) + 0.1 * rng.standard_normal((500, d)) for _ in range(n)], 1)
+    Uj, _ = O.calibrate(K, r)
+    blocks = []
+    for h in range(n):
+        Uh, _ = O.calibrate(K[:, h * d:(h + 1) * d], r // n)
+        blocks.append(Uh)
+    Ub = np.zeros((n * d, r))
+    for h in range(n):
+        Ub[h * d:(h + 1) * d, h * (r // n):(h + 1) * (r // n)] = blocks[h]
+    np.testing.assert_allclose(Ub.T @ Ub, np.eye(r), atol=1e-12)
+    assert O.captured_variance(Uj, K) >= O.captured_variance(Ub, K) * (1 + 1e-3)
