@@ -56,6 +56,8 @@ def parse():
                     help="alg1: pure Algorithm 1 TopK (k = n/8); paper: the paper's serving policy (SURVEY "
                          "§8(f) f4): sink x / recent z forced (16/64 LLaMA, 32/128 Mistral) and layers "
                          "{0, 1, 31} dense (P:515, P:561-564)")
+    ap.add_argument("--v-bits", type=int, default=0, choices=[0, 4, 2],
+                    help="quantised value cache (SURVEY §8(f) f1): 4 or 2 bits, groups of 32 channels")
     ap.add_argument("--separate-append", action="store_true",
                     help="sals_append_latent + sals_decode per layer instead of the fused sals_append_decode")
     return ap.parse_args()
@@ -264,14 +266,24 @@ def run_sals(args, rank, world):
     L, B, s = args.layers, sh["batch"], sh["seq"]
     dev = "cuda"
     pol = policy_of(args.policy, base, L)
-    cfg = sals.make_config(**sh, path=args.path, sink=pol["sink"], recent=pol["recent"])
+    cfg = sals.make_config(**sh, path=args.path, sink=pol["sink"], recent=pol["recent"], v_bits=args.v_bits)
+    cfg_dense = sals.make_config(**sh, path=args.path)
     layers = build_layers(sh, L, dev, synth.SEED_BASE + 1000 * rank,
                           dense=(not args.no_dense) or bool(pol["dense_layers"]))
+    if args.v_bits:   # quantised value rows (synthetic codes, valid bf16 scale / zero per group)
+        rb = sals.sals_v_row_bytes(cfg)
+        nbc = sh["head_dim"] * args.v_bits // 8
+        for ly in layers:
+            vq = torch.randint(0, 256, (B, s, sh["num_kv_heads"], nbc + 16), dtype=torch.uint8, device=dev)
+            par = torch.tensor([0.05, -0.4], dtype=torch.bfloat16, device=dev).view(torch.uint8)
+            vq[..., nbc:] = par.repeat(4)
+            ly["vq"] = vq.view(B, s, rb)
+    vkey = "vq" if args.v_bits else "v"
     D, nqd = sh["num_kv_heads"] * sh["head_dim"], sh["num_q_heads"] * sh["head_dim"]
     seq = torch.full((B,), s, dtype=torch.int32, device=dev)
     pos = seq - 1
     ws = sals.alloc_workspace(sals.sals_workspace_bytes(cfg, B, s), dev)
-    wsd_pol = sals.alloc_workspace(sals.sals_dense_workspace_bytes(cfg, B, s), dev) if pol["dense_layers"] else None
+    wsd_pol = sals.alloc_workspace(sals.sals_dense_workspace_bytes(cfg_dense, B, s), dev) if pol["dense_layers"] else None
     out = torch.empty(L, B, nqd, dtype=torch.bfloat16, device=dev)
 
     def step(sals_only=False):
@@ -279,13 +291,13 @@ def run_sals(args, rank, world):
             if l in pol["dense_layers"]:   # the paper keeps these layers dense
                 if sals_only:
                     continue
-                sals.sals_dense_append(cfg, ly["k_new"], ly["v_new"], pos, ly["k_dense"], ly["v"])
-                sals.sals_dense_decode(cfg, ly["q"], ly["k_dense"], ly["v"], seq, s, out[l], wsd_pol)
+                sals.sals_dense_append(cfg_dense, ly["k_new"], ly["v_new"], pos, ly["k_dense"], ly["v"])
+                sals.sals_dense_decode(cfg_dense, ly["q"], ly["k_dense"], ly["v"], seq, s, out[l], wsd_pol)
             elif args.separate_append:
-                sals.sals_append_latent(cfg, ly["U"], ly["k_new"], ly["v_new"], pos, ly["latent"], ly["v"])
-                sals.sals_decode(cfg, ly["U"], ly["q"], ly["latent"], ly["v"], seq, s, out[l], ws)
+                sals.sals_append_latent(cfg, ly["U"], ly["k_new"], ly["v_new"], pos, ly["latent"], ly[vkey])
+                sals.sals_decode(cfg, ly["U"], ly["q"], ly["latent"], ly[vkey], seq, s, out[l], ws)
             else:   # one projection launch for the append and the query (U read once)
-                sals.sals_append_decode(cfg, ly["U"], ly["k_new"], ly["v_new"], ly["q"], ly["latent"], ly["v"],
+                sals.sals_append_decode(cfg, ly["U"], ly["k_new"], ly["v_new"], ly["q"], ly["latent"], ly[vkey],
                                         seq, s, out[l], ws)
 
     stream = torch.cuda.Stream()
@@ -314,12 +326,12 @@ def run_sals(args, rank, world):
     # ---- dense comparator (same build), same batch / layers
     dense = None
     if not args.no_dense:
-        wsd = sals.alloc_workspace(sals.sals_dense_workspace_bytes(cfg, B, s), dev)
+        wsd = sals.alloc_workspace(sals.sals_dense_workspace_bytes(cfg_dense, B, s), dev)
 
         def dstep():
             for l, ly in enumerate(layers):
-                sals.sals_dense_append(cfg, ly["k_new"], ly["v_new"], pos, ly["k_dense"], ly["v"])
-                sals.sals_dense_decode(cfg, ly["q"], ly["k_dense"], ly["v"], seq, s, out[l], wsd)
+                sals.sals_dense_append(cfg_dense, ly["k_new"], ly["v_new"], pos, ly["k_dense"], ly["v"])
+                sals.sals_dense_decode(cfg_dense, ly["q"], ly["k_dense"], ly["v"], seq, s, out[l], wsd)
         with torch.cuda.stream(stream):
             dstep()
             stream.synchronize()
@@ -335,11 +347,11 @@ def run_sals(args, rank, world):
                  "kernel": "in-build split-K flash decode over the full post-RoPE K/V cache"}
 
     # ---- e2e through the public API with host buffers
-    e2e = run_e2e(cfg, layers, seq, pos, s, ws, out, stream, args, world, pol, wsd_pol)
+    e2e = run_e2e(cfg, layers, seq, pos, s, ws, out, stream, args, world, pol, wsd_pol, cfg_dense, vkey)
 
     # ---- roofline of the dominant kernel
     peaks, peak_kind = load_peaks()
-    roof = roofline(sh, stages, peaks, peak_kind, args.workload)
+    roof = roofline(sh, stages, peaks, peak_kind, args.workload, sals.sals_v_row_bytes(cfg) if args.v_bits else None)
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -351,6 +363,7 @@ def run_sals(args, rank, world):
         "stages_us": stages_us,
         "path": "tcgen05" if stages.get("flash", 0) == 0 else "simt",
         "policy": {k: (list(v) if isinstance(v, tuple) else v) for k, v in pol.items()},
+        "v_bits": args.v_bits or 16,
         "api": "sals_append_latent + sals_decode" if args.separate_append else
                "sals_append_decode (append + query projection in one launch: stage qproj_rope)",
         "roofline": roof,
@@ -499,7 +512,7 @@ def run_sweep(args, rank, world):
         print(json.dumps(line), flush=True)
 
 
-def run_e2e(cfg, layers, seq, pos, s, ws, out, stream, args, world, pol=None, wsd_pol=None):
+def run_e2e(cfg, layers, seq, pos, s, ws, out, stream, args, world, pol=None, wsd_pol=None, cfg_dense=None, vkey="v"):
     from paper_2510_24273_b200 import sals
     L = len(layers)
     B = seq.shape[0]
@@ -516,13 +529,13 @@ def run_e2e(cfg, layers, seq, pos, s, ws, out, stream, args, world, pol=None, ws
             dev_kv.copy_(host_kv, non_blocking=True)
             for l, ly in enumerate(layers):
                 if pol and l in pol["dense_layers"]:
-                    sals.sals_dense_append(cfg, dev_kv[l, 0], dev_kv[l, 1], pos, ly["k_dense"], ly["v"])
-                    sals.sals_dense_decode(cfg, dev_q[l], ly["k_dense"], ly["v"], seq, s, out[l], wsd_pol)
+                    sals.sals_dense_append(cfg_dense, dev_kv[l, 0], dev_kv[l, 1], pos, ly["k_dense"], ly["v"])
+                    sals.sals_dense_decode(cfg_dense, dev_q[l], ly["k_dense"], ly["v"], seq, s, out[l], wsd_pol)
                 elif args.separate_append:
-                    sals.sals_append_latent(cfg, ly["U"], dev_kv[l, 0], dev_kv[l, 1], pos, ly["latent"], ly["v"])
-                    sals.sals_decode(cfg, ly["U"], dev_q[l], ly["latent"], ly["v"], seq, s, out[l], ws)
+                    sals.sals_append_latent(cfg, ly["U"], dev_kv[l, 0], dev_kv[l, 1], pos, ly["latent"], ly[vkey])
+                    sals.sals_decode(cfg, ly["U"], dev_q[l], ly["latent"], ly[vkey], seq, s, out[l], ws)
                 else:
-                    sals.sals_append_decode(cfg, ly["U"], dev_kv[l, 0], dev_kv[l, 1], dev_q[l], ly["latent"], ly["v"],
+                    sals.sals_append_decode(cfg, ly["U"], dev_kv[l, 0], dev_kv[l, 1], dev_q[l], ly["latent"], ly[vkey],
                                             seq, s, out[l], ws)
             host_out.copy_(out, non_blocking=True)
             stream.synchronize()
@@ -543,12 +556,12 @@ def run_e2e(cfg, layers, seq, pos, s, ws, out, stream, args, world, pol=None, ws
                    "stream sync per step"}
 
 
-def roofline(sh, stages, peaks, peak_kind, workload):
+def roofline(sh, stages, peaks, peak_kind, workload, v_row_bytes=None):
     from paper_2510_24273_b200 import traffic
     B, s = sh["batch"], sh["seq"]
     kw = dict(batch=B, seq=s, num_q_heads=sh["num_q_heads"], num_kv_heads=sh["num_kv_heads"],
               head_dim=sh["head_dim"], rank=sh["rank"], score_rank=sh["score_rank"], top_k=sh["top_k"])
-    sb = traffic.stage_bytes(**kw)
+    sb = traffic.stage_bytes(**kw, v_row_bytes=v_row_bytes)
     fl = traffic.recon_flops(**kw)
     hbm = peaks["hbm_gbs"]
     tf = peaks["bf16_tflops"]

@@ -67,7 +67,18 @@ typedef struct {
   int32_t dtype;          /* sals_dtype of every tensor argument                      */
   float   softmax_scale;  /* 0 => 1/sqrt(head_dim) (Alg. 1 line 8)             */
   int32_t path;           /* sals_path                                                */
+  int32_t v_bits;         /* value cache format: 0 or 16 = dtype
+                             values; 4 or 2 = channel-wise group quantised (groups of 32
+                             channels of one token, asymmetric min/max grid, bf16 scale / zero),
+                             bf16 + head_dim 128 + the tcgen05 path only.  Row layout per
+                             token: for every KV head, d*v_bits/8 code bytes (4-bit: two
+                             channels per byte, low nibble first; 2-bit: four, lowest bits
+                             first) then d/32 (bf16 scale, bf16 zero) pairs.  v = zero + scale*code */
 } sals_config;
+
+/* Bytes of one token's row of the value cache (D * sizeof(dtype), or the
+ * quantised layout above).  0 on invalid arguments. */
+size_t sals_v_row_bytes(const sals_config* cfg);
 
 /* Bytes of device workspace sals_decode needs for `batch` requests of at most
  * `max_seq_len` tokens.  0 on invalid arguments. */

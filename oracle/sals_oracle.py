@@ -347,3 +347,41 @@ def captured_variance(U: np.ndarray, K: np.ndarray) -> float:
     """E(U) = ||K U||_F^2 = tr(U^T K^T K U): the key energy kept by the projection (Lemma 1)."""
     KU = np.asarray(K, dtype=np.float64) @ np.asarray(U, dtype=np.float64)
     return float(np.sum(KU * KU))
+
+
+# ------------------------------------------------------------------ value quantisation (f1)
+def bf16_round(x: np.ndarray) -> np.ndarray:
+    """Round to the nearest bfloat16 (ties to even), returned as float64: the storage
+    step of the quantisation parameters (a definition of the format, not arithmetic
+    of the method)."""
+    f = np.asarray(x, dtype=np.float32)
+    u = f.view(np.uint32).astype(np.uint64)
+    lsb = (u >> np.uint64(16)) & np.uint64(1)
+    r = ((u + np.uint64(0x7FFF) + lsb) >> np.uint64(16)) << np.uint64(16)
+    return r.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def quantize_values(v: np.ndarray, bits: int, group: int = 32):
+    """Channel-wise group quantisation of the value cache (KIVI-style
+    asymmetric grid; reading R15): for every token, each run of `group` consecutive
+    channels shares zero = min and scale = (max - min) / (2^bits - 1), both stored
+    in bfloat16; code = clamp(round((v - zero) / scale), 0, 2^bits - 1) computed
+    from the stored (rounded) zero / scale; scale 0 -> code 0.
+    v [..., D] -> (codes [..., D] int, scale [..., D/group], zero [..., D/group])."""
+    v = np.asarray(v, dtype=np.float64)
+    g = v.reshape(*v.shape[:-1], v.shape[-1] // group, group)
+    lo, hi = g.min(-1), g.max(-1)
+    qmax = (1 << bits) - 1
+    zero = bf16_round(lo)
+    scale = bf16_round((hi - lo) / qmax)
+    safe = np.where(scale > 0, scale, 1.0)
+    codes = np.clip(np.rint((g - zero[..., None]) / safe[..., None]), 0, qmax)
+    codes = np.where(scale[..., None] > 0, codes, 0).astype(np.int64)
+    return codes.reshape(v.shape), scale, zero
+
+
+def dequantize_values(codes: np.ndarray, scale: np.ndarray, zero: np.ndarray, group: int = 32) -> np.ndarray:
+    """v^ = zero + scale * code per group (the V^ of Alg. 1)."""
+    c = np.asarray(codes, dtype=np.float64)
+    g = c.reshape(*c.shape[:-1], c.shape[-1] // group, group)
+    return (np.asarray(zero, np.float64)[..., None] + np.asarray(scale, np.float64)[..., None] * g).reshape(c.shape)

@@ -88,6 +88,14 @@ int next_pow2(int v) { int p = 1; while (p < v) p <<= 1; return p; }
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
+// quantised value cache: bits per value (0 = dtype values)
+inline int vq_bits(const sals_config* c) { return (c->v_bits == 4 || c->v_bits == 2) ? c->v_bits : 0; }
+inline size_t v_row_bytes(const sals_config* c) {
+  const int d = c->head_dim, nkv = c->num_kv_heads;
+  if (vq_bits(c)) return (size_t)nkv * ((size_t)d * c->v_bits / 8 + (size_t)(d / 32) * 4);
+  return (size_t)nkv * d * (c->dtype == SALS_BF16 ? 2 : 4);
+}
+
 sals_status validate(const sals_config* c) {
   if (!c) return fail(SALS_ERR_INVALID_ARGUMENT, "cfg is NULL");
   if (c->num_q_heads < 1 || c->num_kv_heads < 1 || c->num_q_heads % c->num_kv_heads)
@@ -116,6 +124,10 @@ sals_status validate(const sals_config* c) {
     return fail(SALS_ERR_INVALID_ARGUMENT, "bad rope_style");
   if (c->softmax_scale < 0.f) return fail(SALS_ERR_INVALID_ARGUMENT, "softmax_scale must be >= 0");
   if (c->path < SALS_PATH_AUTO || c->path > SALS_PATH_TCGEN05) return fail(SALS_ERR_INVALID_ARGUMENT, "bad path");
+  if (c->v_bits != 0 && c->v_bits != 16 && c->v_bits != 4 && c->v_bits != 2)
+    return fail(SALS_ERR_INVALID_ARGUMENT, "v_bits %d not in {0, 16, 4, 2}", c->v_bits);
+  if (vq_bits(c) && (c->dtype != SALS_BF16 || d != 128))
+    return fail(SALS_ERR_UNSUPPORTED, "quantised values need bf16 and head_dim 128");
   return SALS_OK;
 }
 
@@ -228,6 +240,8 @@ sals_status make_plan(const sals_config* c, int batch, int max_s, Plan& p, bool 
   if (c->path == SALS_PATH_TCGEN05 && !p.tc && !for_size)
     return fail(SALS_ERR_UNSUPPORTED, "tcgen05 path needs bf16, B*k >= 128, d in {64,128,256}, D %% 256 == 0");
   p.tc2 = p.tc && tc2_supported(c->head_dim, p.D, c->rank, p.G);
+  if (vq_bits(c) && !p.tc2 && !for_size)
+    return fail(SALS_ERR_UNSUPPORTED, "quantised values need the tcgen05 v2 path (bf16, d = 128, B*k >= 128)");
   if (p.tc2) {
     const int ntiles = ceil_div(p.kmax, kTcRows);
     const int64_t units = (int64_t)batch * (p.D / 256) * ntiles;
@@ -413,6 +427,7 @@ sals_status attend_list(const sals_config* c, const Plan& p, const void* U, cons
   if (p.tc) {
     TcArgs t{};
     t.latent = latent; t.cap = cap; t.r = c->rank; t.U = U; t.v_cache = v_cache;
+    t.v_bits = vq_bits(c); t.v_row_bytes = (int)v_row_bytes(c);
     t.sel = sel; t.count = count; t.k_stride = c->top_k; t.D = p.D; t.head_dim = c->head_dim;
     t.G = p.G; t.n_q = c->num_q_heads; t.pos_base = pos_base; t.rope = make_rope(c);
     t.qrope = qrope; t.scale_log2 = scale_log2(c); t.partials = part; t.ntiles = p.nsplit;
@@ -486,6 +501,7 @@ sals_status decode_impl(const sals_config* c, const void* U, const void* q, cons
   sals_status s = SALS_OK;
   if (fused) {
     pa.xa = k_new; pa.ncols_a = c->rank; pa.v_new = v_new; pa.pos = nullptr;
+    pa.v_bits = vq_bits(c); pa.v_row_bytes = (int)v_row_bytes(c);
     pa.latent = const_cast<void*>(latent); pa.v_cache = const_cast<void*>(v_cache); pa.cap = cap;
     Plan pf = p;
     plan_proj(pf, false);   // the append's cluster shape (more column blocks)
@@ -536,6 +552,11 @@ const char* sals_status_string(sals_status s) {
 
 const char* sals_last_error(void) { return g_err.c_str(); }
 
+size_t sals_v_row_bytes(const sals_config* cfg) {
+  if (validate(cfg) != SALS_OK) return 0;
+  return v_row_bytes(cfg);
+}
+
 uint32_t sals_profile_stage_mask(uint32_t mask) {
   const uint32_t old = g_stage_mask;
   g_stage_mask = mask;
@@ -568,6 +589,7 @@ sals_status sals_append_latent(const sals_config* cfg, const void* U, const void
   a.U = U; a.x = k_new; a.x_stride = p.D; a.D = p.D; a.r = cfg->rank; a.ncols = cfg->rank; a.B = batch;
   a.head_dim = cfg->head_dim; a.group = 1; a.n_q = cfg->num_q_heads; a.latent = latent_cache; a.cap = cap;
   a.pos = d_pos; a.v_new = v_new; a.v_cache = v_cache;
+  a.v_bits = vq_bits(cfg); a.v_row_bytes = (int)v_row_bytes(cfg);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (!on(kNumStages)) return SALS_OK;
   if (cfg->dtype == SALS_BF16) return launch_project<__nv_bfloat16>(cfg, p, 0, a, st);

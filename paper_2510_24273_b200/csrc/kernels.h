@@ -38,6 +38,7 @@ struct ProjectArgs {
   // fused append + query projection (MODE 2): append role's input / columns / block count;
   // pos == nullptr -> the new token's slot is seq_len[b] - 1
   const void* xa; int ncols_a; int n_append_blocks;
+  int v_bits, v_row_bytes;   // value row format (0: dtype values; 4 / 2: quantised, head_dim 128)
 };
 
 struct ScoreArgs {

@@ -119,16 +119,53 @@ project_kernel(ProjectArgs a) {
   }
 
   if (!pool && a.v_new != nullptr) {
-    // ---- append: copy v_new[b] -> v_cache[b, pos_b] (16-byte vectors) ----
-    const int nvec = a.D * (int)sizeof(T) / 16;
     const int ncta = CS * (MODE == 2 ? a.n_append_blocks : (int)gridDim.y);
     const int cta = blockIdx.y * CS + rank;
-    for (int i = cta * kProjThreads + tid; i < a.B * nvec; i += ncta * kProjThreads) {
-      const int b = i / nvec, v = i % nvec;
-      const uint4 val = ld_v4(reinterpret_cast<const char*>(a.v_new) + ((size_t)b * a.D) * sizeof(T) + v * 16);
-      const int pb = a.pos ? a.pos[b] : a.seq_len[b] - 1;
-      *reinterpret_cast<uint4*>(reinterpret_cast<char*>(a.v_cache) +
-                                (((size_t)b * a.cap + pb) * a.D) * sizeof(T) + v * 16) = val;
+    if (a.v_bits == 0) {
+      // ---- append: copy v_new[b] -> v_cache[b, pos_b] (16-byte vectors) ----
+      const int nvec = a.D * (int)sizeof(T) / 16;
+      for (int i = cta * kProjThreads + tid; i < a.B * nvec; i += ncta * kProjThreads) {
+        const int b = i / nvec, v = i % nvec;
+        const uint4 val = ld_v4(reinterpret_cast<const char*>(a.v_new) + ((size_t)b * a.D) * sizeof(T) + v * 16);
+        const int pb = a.pos ? a.pos[b] : a.seq_len[b] - 1;
+        *reinterpret_cast<uint4*>(reinterpret_cast<char*>(a.v_cache) +
+                                  (((size_t)b * a.cap + pb) * a.D) * sizeof(T) + v * 16) = val;
+      }
+    } else {
+      // ---- append with channel-wise group quantisation (DESIGN R15): one
+      // thread per (request, group of 32 channels); zero = min, scale = (max-min)/qmax,
+      // both rounded to bf16 first, codes from the rounded values, packed low bits first
+      const int bits = a.v_bits, qmax = (1 << bits) - 1;
+      const int gph = 128 / 32;                       // groups per head (head_dim 128)
+      const int hb = 128 * bits / 8 + gph * 4;        // bytes per head in a row
+      const int ngroups = a.D / 32;
+      for (int i = cta * kProjThreads + tid; i < a.B * ngroups; i += ncta * kProjThreads) {
+        const int b = i / ngroups, gi = i - b * ngroups, h = gi / gph, gq = gi - h * gph;
+        const char* src = reinterpret_cast<const char*>(a.v_new) + ((size_t)b * a.D + gi * 32) * 2;
+        float f[32];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) Elem<__nv_bfloat16>::unpack(ld_v4(src + 16 * q), f + 8 * q);
+        float lo = f[0], hi = f[0];
+#pragma unroll
+        for (int e = 1; e < 32; ++e) { lo = fminf(lo, f[e]); hi = fmaxf(hi, f[e]); }
+        const __nv_bfloat16 zb = __float2bfloat16_rn(lo);
+        const __nv_bfloat16 sb = __float2bfloat16_rn(__fdiv_rn(hi - lo, (float)qmax));
+        const float zf = __bfloat162float(zb), sf = __bfloat162float(sb);
+        const int pb = a.pos ? a.pos[b] : a.seq_len[b] - 1;
+        char* row = reinterpret_cast<char*>(a.v_cache) + ((size_t)b * a.cap + pb) * a.v_row_bytes + (size_t)h * hb;
+        uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          int c = 0;
+          if (sf > 0.f) c = min(qmax, max(0, __float2int_rn(__fdiv_rn(f[e] - zf, sf))));
+          const int bitpos = e * bits;
+          w[bitpos >> 5] |= (uint32_t)c << (bitpos & 31);
+        }
+        if (bits == 4) *reinterpret_cast<uint4*>(row + gq * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+        else *reinterpret_cast<uint2*>(row + gq * 8) = make_uint2(w[0], w[1]);
+        const uint32_t par = (uint32_t)__bfloat16_as_ushort(sb) | ((uint32_t)__bfloat16_as_ushort(zb) << 16);
+        *reinterpret_cast<uint32_t*>(row + 128 * bits / 8 + gq * 4) = par;
+      }
     }
   }
 

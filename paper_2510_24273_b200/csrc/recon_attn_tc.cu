@@ -449,12 +449,18 @@ sals_status launch_recon_attn_tc(const TcArgs& a, int batch, cudaStream_t st) {
     if (rows > 0x7fffffffull) { g_tc_err = "B*cap exceeds the 2^31 rows of a TMA gather"; return SALS_ERR_UNSUPPORTED; }
     cuuint64_t dl[2] = {(cuuint64_t)a.r, rows}, sl[1] = {(cuuint64_t)a.r * 2};
     cuuint32_t bl[2] = {64, 1};
-    cuuint64_t dv[2] = {(cuuint64_t)a.D, rows}, sv[1] = {(cuuint64_t)a.D * 2};
-    cuuint32_t bv[2] = {256, 1};
+    // value rows: bf16 [D] per token (256-column boxes), or the quantised byte rows
+    // (2 heads' code + parameter bytes per box, DESIGN R15)
+    const bool vq = a.v_bits != 0;
+    const int vhead = vq ? 128 * a.v_bits / 8 + 16 : 0;
+    cuuint64_t dv[2] = {vq ? (cuuint64_t)a.v_row_bytes : (cuuint64_t)a.D, rows};
+    cuuint64_t sv[1] = {vq ? (cuuint64_t)a.v_row_bytes : (cuuint64_t)a.D * 2};
+    cuuint32_t bv[2] = {vq ? (cuuint32_t)(2 * vhead) : 256u, 1};
     if (g_encode(&ml, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a.latent), dl, sl, bl, estr,
                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
-        g_encode(&mv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a.v_cache), dv, sv, bv, estr,
+        g_encode(&mv, vq ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                 const_cast<void*>(a.v_cache), dv, sv, bv, estr,
                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
       g_tc_err = "cuTensorMapEncodeTiled failed for the gather maps";

@@ -24,6 +24,8 @@ struct TcArgs {
                           // several with `counters` (the last chunk CTA of a (request, column
                           // block) merges the partials, deterministic split order)
   unsigned* counters;     // v2, nullable: [B, D/256] arrival counters, zero on entry
+  int v_bits;             // 0: dtype values; 4 / 2: quantised value rows (v2 only)
+  int v_row_bytes;        // bytes of one token's value row
 };
 
 bool tc_supported(int head_dim, int D, int rank, int G);

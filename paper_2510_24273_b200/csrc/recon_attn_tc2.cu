@@ -222,11 +222,15 @@ __device__ unsigned long long g_trace[128];
 #define TSTAMP(slot) do {} while (0)
 #endif
 
-template <int G, int STYLE>
+// VB: 16 = dtype (bf16) value rows; 4 / 2 = quantised value rows (DESIGN R15):
+// per KV head 128*VB/8 code bytes then 4 (bf16 scale, bf16 zero) pairs.
+template <int G, int STYLE, int VB>
 __global__ void __launch_bounds__(kThreads, 1)
 recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_constant__ CUtensorMap tmap_lat,
                       const __grid_constant__ CUtensorMap tmap_v, const __grid_constant__ KArgs ka) {
   constexpr int NQH = 2 * G;             // query heads of this CTA (2 KV heads)
+  constexpr int kVHead = VB == 16 ? kDH * 2 : kDH * VB / 8 + (kDH / 32) * 4;   // value bytes per head-token
+  constexpr int kVRow = 2 * kVHead;                                           // bytes of a V tile row (2 heads)
   const TcArgs& a = ka.a;
   extern __shared__ uint8_t smem_raw[];
   // align with pointer arithmetic on the __shared__ array so the compiler keeps the shared
@@ -365,9 +369,9 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
         idx[t] = t < nv ? b * (int)a.cap + selb[tile * kRows + t] : -1;
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive_expect_tx(vfull, (uint32_t)kVBytes);
+      if (lane == 0) mbar_arrive_expect_tx(vfull, (uint32_t)(kRows * kVRow));
       __syncwarp();
-      tma_gather4(smem_u32(sV + lane * 4 * (kBN * 2)), &tmap_v, n0, idx[4 * lane], idx[4 * lane + 1],
+      tma_gather4(smem_u32(sV + lane * 4 * kVRow), &tmap_v, VB == 16 ? n0 : nb * kVRow, idx[4 * lane], idx[4 * lane + 1],
                   idx[4 * lane + 2], idx[4 * lane + 3], vfull);
       if (it + 1 < ntile) {   // next tile's V rows -> L2 via the LSU (keeps the TMA queue for loads)
         const int ntl = tile + 1;
@@ -376,9 +380,10 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
         for (int j = 0; j < 4; ++j) {
           const int t = lane + 32 * j;
           if (t < nnv) {
-            const char* vr = vb + (((size_t)b * a.cap + selb[ntl * kRows + t]) * a.D + n0) * 2;
+            const char* vr = VB == 16 ? vb + (((size_t)b * a.cap + selb[ntl * kRows + t]) * a.D + n0) * 2
+                                      : vb + ((size_t)b * a.cap + selb[ntl * kRows + t]) * a.v_row_bytes + nb * kVRow;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) prefetch_l2(vr + c * 128);
+            for (int c = 0; c < (kVRow + 127) / 128; ++c) prefetch_l2(vr + c * 128);
           }
         }
       }
@@ -549,7 +554,8 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
 #pragma unroll
           for (int e = 0; e < 4; ++e) { ov[g][e].x *= al[g]; ov[g][e].y *= al[g]; }
         }
-        const uint4* vrow = reinterpret_cast<const uint4*>(sV) + lane;   // row t at vrow[t * 32]
+        const uint4* vrow = reinterpret_cast<const uint4*>(sV) + lane;   // (VB 16) row t at vrow[t * 32]
+        const uint8_t* qrow = sV + kh * kVHead;                            // (quantised) row t at qrow[t * kVRow]
         const float* pp = sP + kh * G * kPS;
         const int tb = 16 * ew;
 #pragma unroll
@@ -562,17 +568,33 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             if (t0 + j < nv) {
-              const uint4 v = vrow[(t0 + j) * 32];
-              const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+              float2 vv[4];   // the lane's 8 values (dims 8 (lane & 15) .. + 8 of KV head kh)
+              if constexpr (VB == 16) {
+                const uint4 v = vrow[(t0 + j) * 32];
+                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) vv[e] = make_float2(__uint_as_float(w[e] << 16), __uint_as_float(w[e] & 0xffff0000u));
+              } else {
+                const uint8_t* rq = qrow + (t0 + j) * kVRow;
+                const int l8 = lane & 15;
+                const uint32_t par = *reinterpret_cast<const uint32_t*>(rq + 128 * VB / 8 + 4 * (l8 >> 2));
+                const float sf = __uint_as_float(par << 16), zf = __uint_as_float(par & 0xffff0000u);
+                uint32_t cw;
+                if constexpr (VB == 4) cw = *reinterpret_cast<const uint32_t*>(rq + 4 * l8);
+                else cw = *reinterpret_cast<const uint16_t*>(rq + 2 * l8);
+                constexpr uint32_t m = (1u << VB) - 1;
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  vv[e] = make_float2(fmaf(sf, (float)((cw >> (2 * e * VB)) & m), zf),
+                                      fmaf(sf, (float)((cw >> ((2 * e + 1) * VB)) & m), zf));
+              }
 #pragma unroll
               for (int g = 0; g < G; ++g) {
                 const float pj = j == 0 ? p4[g].x : j == 1 ? p4[g].y : j == 2 ? p4[g].z : p4[g].w;
                 lp[g] += pj;
                 const float2 p2 = make_float2(pj, pj);
 #pragma unroll
-                for (int e = 0; e < 4; ++e)
-                  ov[g][e] = __ffma2_rn(p2, make_float2(__uint_as_float(w[e] << 16), __uint_as_float(w[e] & 0xffff0000u)),
-                                        ov[g][e]);
+                for (int e = 0; e < 4; ++e) ov[g][e] = __ffma2_rn(p2, vv[e], ov[g][e]);
               }
             }
           }
@@ -636,10 +658,10 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
   pdl_launch_dependents();
 }
 
-template <int G, int STYLE>
+template <int G, int STYLE, int VB>
 cudaError_t launch_t(const CUtensorMap& map, const CUtensorMap& map_lat, const CUtensorMap& map_v, const TcArgs& a,
                      int batch, cudaStream_t st) {
-  auto kern = recon_attn_tc2_kernel<G, STYLE>;
+  auto kern = recon_attn_tc2_kernel<G, STYLE, VB>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(G));
@@ -683,12 +705,17 @@ bool tc2_supported(int head_dim, int D, int rank, int G) {
 cudaError_t launch_recon_attn_tc2(const CUtensorMap& map, const CUtensorMap& ml, const CUtensorMap& mv,
                                   const TcArgs& a, int batch, cudaStream_t st) {
   const int style = a.rope.style;
-  switch (a.G) {
-    case 1: return style ? tc2::launch_t<1, 1>(map, ml, mv, a, batch, st) : tc2::launch_t<1, 0>(map, ml, mv, a, batch, st);
-    case 2: return style ? tc2::launch_t<2, 1>(map, ml, mv, a, batch, st) : tc2::launch_t<2, 0>(map, ml, mv, a, batch, st);
-    case 4: return style ? tc2::launch_t<4, 1>(map, ml, mv, a, batch, st) : tc2::launch_t<4, 0>(map, ml, mv, a, batch, st);
-  }
+#define SALS_TC2_VB(VB)                                                                                         \
+  switch (a.G) {                                                                                                \
+    case 1: return style ? tc2::launch_t<1, 1, VB>(map, ml, mv, a, batch, st) : tc2::launch_t<1, 0, VB>(map, ml, mv, a, batch, st); \
+    case 2: return style ? tc2::launch_t<2, 1, VB>(map, ml, mv, a, batch, st) : tc2::launch_t<2, 0, VB>(map, ml, mv, a, batch, st); \
+    case 4: return style ? tc2::launch_t<4, 1, VB>(map, ml, mv, a, batch, st) : tc2::launch_t<4, 0, VB>(map, ml, mv, a, batch, st); \
+  }                                                                                                             \
   return cudaErrorInvalidValue;
+  if (a.v_bits == 4) { SALS_TC2_VB(4) }
+  if (a.v_bits == 2) { SALS_TC2_VB(2) }
+  SALS_TC2_VB(16)
+#undef SALS_TC2_VB
 }
 
 }  // namespace sals

@@ -24,7 +24,8 @@ EXPORTED = ["sals_workspace_bytes", "sals_append_latent", "sals_decode", "sals_d
             "sals_dense_workspace_bytes", "sals_dense_decode", "sals_shard_candidates", "sals_shard_attend",
             "sals_merge_partials", "sals_shard_workspace_bytes", "sals_status_string", "sals_last_error",
             "sals_launch_count", "sals_profile_stage_mask", "sals_append_decode",
-            "sals_append_latent_bulk", "sals_calibrate_workspace_bytes", "sals_calibrate"]
+            "sals_append_latent_bulk", "sals_calibrate_workspace_bytes", "sals_calibrate",
+            "sals_v_row_bytes"]
 
 
 class SalsError(RuntimeError):
@@ -38,15 +39,15 @@ class sals_config(ctypes.Structure):
                 ("rank", ctypes.c_int32), ("score_rank", ctypes.c_int32), ("top_k", ctypes.c_int32),
                 ("sink", ctypes.c_int32), ("recent", ctypes.c_int32), ("rope_base", ctypes.c_float),
                 ("rope_style", ctypes.c_int32), ("dtype", ctypes.c_int32), ("softmax_scale", ctypes.c_float),
-                ("path", ctypes.c_int32)]
+                ("path", ctypes.c_int32), ("v_bits", ctypes.c_int32)]
 
 
 def make_config(*, num_q_heads, num_kv_heads, head_dim, rank, score_rank, top_k, sink=0, recent=0,
                 rope_base=10000.0, rope_style=SALS_ROPE_HALF, dtype="bf16", softmax_scale=0.0,
-                path=SALS_PATH_AUTO, **_unused) -> sals_config:
+                path=SALS_PATH_AUTO, v_bits=0, **_unused) -> sals_config:
     dt = {"bf16": SALS_BF16, "f32": SALS_F32, torch.bfloat16: SALS_BF16, torch.float32: SALS_F32}[dtype]
     return sals_config(num_q_heads, num_kv_heads, head_dim, rank, score_rank, top_k, sink, recent,
-                       float(rope_base), rope_style, dt, float(softmax_scale), path)
+                       float(rope_base), rope_style, dt, float(softmax_scale), path, int(v_bits))
 
 
 def torch_dtype(cfg: sals_config):
@@ -67,6 +68,7 @@ def _load():
         "sals_append_decode": (I32, [C, P, P, P, P, P, P, I64, I32, P, I32, P, P, P, P, SZ, P]),
         "sals_append_latent_bulk": (I32, [C, P, P, P, I32, I32, I64, P, P, I64, P]),
         "sals_calibrate_workspace_bytes": (SZ, [C]),
+        "sals_v_row_bytes": (SZ, [C]),
         "sals_calibrate": (I32, [C, P, I64, P, P, P, SZ, P]),
         "sals_decode_profile": (I32, [C, P, P, P, P, I64, I32, P, I32, P, P, SZ, I32, P, P]),
         "sals_dense_append": (I32, [C, P, P, I32, P, P, P, I64, P]),
@@ -135,6 +137,11 @@ def sals_decode(cfg, U, q, latent_cache, v_cache, seq_len, max_seq_len, out, wor
 
 
 STAGES = ["qproj_rope", "score", "topk", "recon_attn", "flash", "merge"]
+
+
+def sals_v_row_bytes(cfg) -> int:
+    """Bytes of one token's value-cache row (D * dtype size, or the quantised layout of cfg.v_bits)."""
+    return int(_lib.sals_v_row_bytes(ctypes.byref(cfg)))
 
 
 def sals_calibrate_workspace_bytes(cfg) -> int:

@@ -20,7 +20,7 @@ def sals_speedup(d_rstar: float, d_r: float, k_s: float) -> float:
 
 
 def stage_bytes(*, batch, seq, num_q_heads, num_kv_heads, head_dim, rank, score_rank, top_k,
-                elem=2, **_):
+                elem=2, v_row_bytes=None, **_):
     """Algorithmic HBM bytes per layer-step of each stage (whole batch).
 
     seq = s (tokens incl. the decoded one); k_eff = min(k, s).
@@ -33,7 +33,8 @@ def stage_bytes(*, batch, seq, num_q_heads, num_kv_heads, head_dim, rank, score_
     b["score"] = batch * seq * score_rank * elem + batch * seq * 4          # latent reads + fp32 scores
     b["topk"] = batch * seq * 4 + batch * k * 4                               # scores (L2) + indices
     # fused reconstruct+attention: gathered latent rows, U once, gathered V rows, partials
-    b["recon_attn"] = batch * k * rank * elem + rank * D * elem + batch * k * D * elem
+    vrow = v_row_bytes if v_row_bytes else D * elem      # quantised value rows (f1) are smaller
+    b["recon_attn"] = batch * k * rank * elem + rank * D * elem + batch * k * vrow
     b["total"] = b["append"] + b["qproj"] + b["score"] + b["recon_attn"]
     return b
 

@@ -351,3 +351,84 @@ def test_calibrate_matches_oracle():
     Uo, wo = O.calibrate(H.widen(Kd), r)
     np.testing.assert_allclose(H.widen(w), wo, rtol=2e-4, atol=1e-3 * wo[0] * 1e-3)
     np.testing.assert_allclose(H.widen(U), Uo, atol=2e-3)
+
+
+# ------------------------------------------------------------------ quantised value cache (f1)
+def _pack_values(v, bits, nkv):
+    """The library's quantised row format (include/sals.h, cfg.v_bits), written with the
+    oracle's quantiser: per KV head 128*bits/8 code bytes (low bits first) + 4 x (bf16
+    scale, bf16 zero)."""
+    codes, scale, zero = O.quantize_values(v, bits, 32)          # [..., D], [..., D/32]
+    lead = v.shape[:-1]
+    per = 8 // bits
+    c = codes.reshape(*lead, nkv, 128 // per, per)
+    packed = np.zeros((*lead, nkv, 128 // per), dtype=np.uint8)
+    for e in range(per):
+        packed |= (c[..., e] << (e * bits)).astype(np.uint8)
+    sb = torch.from_numpy(scale.astype(np.float32)).bfloat16().view(torch.int16).numpy().view(np.uint16)
+    zb = torch.from_numpy(zero.astype(np.float32)).bfloat16().view(torch.int16).numpy().view(np.uint16)
+    par = np.stack([sb, zb], -1).reshape(*lead, nkv, 4, 2).view(np.uint8).reshape(*lead, nkv, 16)
+    return np.concatenate([packed, par], -1).reshape(*lead, -1)
+
+
+def _unpack_values(rows, bits, nkv):
+    """Inverse of _pack_values: the stored codes / scale / zero -> V^ (fp64)."""
+    lead = rows.shape[:-1]
+    r = rows.reshape(*lead, nkv, -1)
+    nb = 128 * bits // 8
+    per = 8 // bits
+    cb = r[..., :nb].astype(np.int64)
+    codes = np.stack([(cb >> (e * bits)) & ((1 << bits) - 1) for e in range(per)], -1).reshape(*lead, nkv, 128)
+    par = np.ascontiguousarray(r[..., nb:nb + 16]).view(np.uint16).reshape(*lead, nkv, 4, 2)
+    to_f = lambda u: torch.from_numpy(u.astype(np.int16)).view(torch.bfloat16).float().numpy().astype(np.float64)
+    scale, zero = to_f(par[..., 0]), to_f(par[..., 1])
+    return O.dequantize_values(codes.reshape(*lead, nkv * 128), scale.reshape(*lead, -1), zero.reshape(*lead, -1), 32)
+
+
+@pytest.mark.parametrize("bits,nkv,G", [(4, 8, 4), (2, 8, 4), (4, 4, 1)])
+def test_quantized_values_decode(bits, nkv, G):
+    """Quantised value cache: the append quantises v_new like the oracle (codes within 1
+    step, identical bf16 parameters in almost every group), and the decode over the
+    stored rows equals the oracle's Algorithm 1 with V replaced by the stored V^
+    (selection in the band, bf16 output tolerances)."""
+    from paper_2510_24273_b200 import sals
+    d, B, seqs, k = 128, 2, [3000, 2311], 384
+    D = nkv * d
+    sh = dict(num_q_heads=nkv * G, num_kv_heads=nkv, head_dim=d, rank=256, score_rank=128, top_k=k,
+              rope_base=1e6, dtype="bf16")
+    cfg = sals.make_config(**sh, v_bits=bits)
+    row_bytes = sals.sals_v_row_bytes(cfg)
+    assert row_bytes == nkv * (128 * bits // 8 + 16)
+    p = synth.gen_problem(num_q_heads=nkv * G, num_kv_heads=nkv, head_dim=d, rank=256, batch=B, seq_lens=seqs, seed=21)
+    dev = lambda a: torch.from_numpy(a).cuda().bfloat16()
+    U, q, kn, vn, lat = dev(p["U"]), dev(p["q"]), dev(p["k_new"]), dev(p["v_new"]), dev(p["latent"])
+    v_host = H.widen(dev(p["v"]))                                   # the bf16 values the cache quantises
+    vq = torch.from_numpy(_pack_values(v_host, bits, nkv)).cuda()    # [B, cap, row_bytes] uint8
+    s_max = max(seqs)
+    seq = torch.tensor(seqs, dtype=torch.int32, device="cuda")
+    ws = sals.alloc_workspace(sals.sals_workspace_bytes(cfg, B, s_max), "cuda")
+    out = torch.empty(B, nkv * G * d, dtype=torch.bfloat16, device="cuda")
+    sel = torch.full((B, k), -7, dtype=torch.int32, device="cuda")
+    scores = torch.zeros(B, s_max, dtype=torch.float32, device="cuda")
+    sals.sals_append_decode(cfg, U, kn, vn, q, lat, vq, seq, s_max, out, ws, sel_idx_out=sel, scores_out=scores)
+    torch.cuda.synchronize()
+    rows = vq.cpu().numpy()
+    # append: the new token's row vs the oracle's quantisation of v_new
+    for b in range(B):
+        got = rows[b, seqs[b] - 1]
+        ref = _pack_values(H.widen(vn[b:b + 1]), bits, nkv)[0]
+        gv, rv = _unpack_values(got[None], bits, nkv)[0], _unpack_values(ref[None], bits, nkv)[0]
+        _, sc_ref, _ = O.quantize_values(H.widen(vn[b:b + 1]), bits, 32)
+        assert np.all(np.abs(gv - rv) <= sc_ref.repeat(32, -1)[0] * 1.01 + 1e-6)
+    # decode vs the oracle over the stored V^ (cache mode)
+    vhat = _unpack_values(rows, bits, nkv)
+    oc = H.oracle_cfg(sh)
+    host_lat = H.widen(lat)
+    orc = O.decode(oc, H.widen(U), H.widen(q), host_lat, vhat, np.array(seqs))
+    forced = []
+    for b in range(B):
+        H.check_selection(orc["scores"][b], orc["sel"][b], sel.cpu().numpy()[b], seqs[b], k, 0, 0)
+        srow = sel.cpu().numpy()[b]
+        forced.append(srow[srow >= 0].astype(np.int64))
+    orc_f = O.decode(oc, H.widen(U), H.widen(q), host_lat, vhat, np.array(seqs), forced_selection=forced)
+    H.check_output(H.widen(out), orc_f["y"], "bf16")

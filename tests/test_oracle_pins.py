@@ -393,3 +393,43 @@ def test_lemma1_joint_projection_captures_at_least_per_head():
         Ub[h * d:(h + 1) * d, h * (r // n):(h + 1) * (r // n)] = blocks[h]
     np.testing.assert_allclose(Ub.T @ Ub, np.eye(r), atol=1e-12)
     assert O.captured_variance(Uj, K) >= O.captured_variance(Ub, K) * (1 + 1e-3)
+
+
+# ------------------------------------------------------------------ value quantisation (f1)
+@pytest.mark.parametrize("bits", [2, 4, 8])
+def test_quantize_values_grid(bits):
+    """Every group's min and max are on the grid (codes 0 and 2^b - 1 up to the bf16
+    storage of zero / scale), every element is within half a step (+ the storage
+    rounding) of its reconstruction, and values already on a representable grid
+    round-trip exactly."""
+    rng = np.random.default_rng(bits)
+    v = rng.standard_normal((5, 3, 64))
+    codes, scale, zero = O.quantize_values(v, bits, 32)
+    qmax = (1 << bits) - 1
+    assert codes.min() >= 0 and codes.max() <= qmax
+    vh = O.dequantize_values(codes, scale, zero, 32)
+    g = v.reshape(5, 3, 2, 32)
+    step = scale[..., None]
+    err = np.abs(vh.reshape(5, 3, 2, 32) - g)
+    # half a step + the bf16 rounding of zero (<= 2^-9 |min|) and of scale (x qmax)
+    bound = 0.5 * step + 2.0 ** -8 * (np.abs(g.min(-1))[..., None] + qmax * step) + 1e-12
+    assert np.all(err <= bound)
+    # exact grid: zero / scale representable in bf16, values = zero + scale * code
+    c = rng.integers(0, qmax + 1, size=(4, 32))
+    c[:, 0], c[:, 1] = 0, qmax
+    vg = -1.5 + 0.125 * c
+    codes2, s2, z2 = O.quantize_values(vg, bits, 32)
+    np.testing.assert_array_equal(codes2, c)
+    np.testing.assert_array_equal(O.dequantize_values(codes2, s2, z2, 32), vg)
+
+
+def test_quantize_constant_group_and_bf16_round():
+    """A constant group has scale 0 and code 0 and reconstructs to its value (bf16);
+    bf16_round matches hand-computed roundings (ties to even)."""
+    v = np.full((1, 32), 0.3)
+    codes, scale, zero = O.quantize_values(v, 4, 32)
+    assert scale[0, 0] == 0 and np.all(codes == 0)
+    np.testing.assert_allclose(O.dequantize_values(codes, scale, zero, 32), O.bf16_round(v))
+    # 1 + 2^-8 is a tie between 1 and 1 + 2^-7: ties to even -> 1; 1 + 3*2^-8 -> 1 + 2^-6
+    np.testing.assert_array_equal(O.bf16_round(np.array([1 + 2.0 ** -8, 1 + 3 * 2.0 ** -8, -2.0])),
+                                  [1.0, 1 + 2.0 ** -6, -2.0])
