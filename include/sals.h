@@ -94,7 +94,8 @@ size_t sals_workspace_bytes(const sals_config* cfg, int32_t batch, int32_t max_s
  *   v_new        [B, D]       values of the new token
  *   d_pos        [B] int32    device: slot (= absolute position) of the new token, 0 <= pos < cap
  *   latent_cache [B, cap, r]  written in place (row d_pos[b] only)
- *   v_cache      [B, cap, D]  written in place (row d_pos[b] only)
+ *   v_cache      [B, cap, D]  written in place (row d_pos[b] only); with cfg->v_bits 4 / 2:
+ *                [B, cap, sals_v_row_bytes(cfg)] bytes, v_new quantised into the row
  * Must precede sals_decode of the same step on the same stream (Alg. 1 appends
  * before scoring).
  */
@@ -116,7 +117,7 @@ sals_status sals_append_latent(const sals_config* cfg, const void* U, const void
  *   U            [D, r]
  *   q            [B, n_q*d]       PRE-RoPE queries of the decoded token
  *   latent_cache [B, cap, r]      rows 0..s_b-1 valid (append already done)
- *   v_cache      [B, cap, D]
+ *   v_cache      [B, cap, D]      (or [B, cap, sals_v_row_bytes(cfg)] bytes with cfg->v_bits 4 / 2)
  *   d_seq_len    [B] int32        device: s_b, 1 <= s_b <= min(cap, max_seq_len)
  *   max_seq_len  host upper bound of every s_b (sizes grids; no device read)
  *   out          [B, n_q*d]       attention output y
