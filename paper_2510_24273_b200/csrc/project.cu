@@ -132,39 +132,45 @@ project_kernel(ProjectArgs a) {
                                   (((size_t)b * a.cap + pb) * a.D) * sizeof(T) + v * 16) = val;
       }
     } else {
-      // ---- append with channel-wise group quantisation (DESIGN R15): one
-      // thread per (request, group of 32 channels); zero = min, scale = (max-min)/qmax,
-      // both rounded to bf16 first, codes from the rounded values, packed low bits first
+      // ---- append with channel-wise group quantisation (DESIGN R15): four
+      // lanes per 32-channel group (8 channels each, one 16-byte load), min / max by
+      // two shuffles; zero = min, scale = (max-min)/qmax, both rounded to bf16 first,
+      // codes from the rounded values (x 1/scale), packed low bits first
       const int bits = a.v_bits, qmax = (1 << bits) - 1;
       const int gph = 128 / 32;                       // groups per head (head_dim 128)
       const int hb = 128 * bits / 8 + gph * 4;        // bytes per head in a row
-      const int ngroups = a.D / 32;
-      for (int i = cta * kProjThreads + tid; i < a.B * ngroups; i += ncta * kProjThreads) {
-        const int b = i / ngroups, gi = i - b * ngroups, h = gi / gph, gq = gi - h * gph;
-        const char* src = reinterpret_cast<const char*>(a.v_new) + ((size_t)b * a.D + gi * 32) * 2;
-        float f[32];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) Elem<__nv_bfloat16>::unpack(ld_v4(src + 16 * q), f + 8 * q);
+      const int nitems = a.B * (a.D / 8);             // (request, 8-channel slice); 4 per group, lane-adjacent
+      for (int i0 = cta * kProjThreads; i0 < nitems; i0 += ncta * kProjThreads) {
+        const int i = i0 + tid;
+        const bool ok = i < nitems;
+        const int b = ok ? i / (a.D / 8) : 0, sl = ok ? i - b * (a.D / 8) : 0;
+        const int gi = sl >> 2, q = sl & 3, h = gi / gph, gq = gi - h * gph;
+        float f[8];
+        if (ok) Elem<__nv_bfloat16>::unpack(ld_v4(reinterpret_cast<const char*>(a.v_new) + ((size_t)b * a.D + sl * 8) * 2), f);
+        else for (int e = 0; e < 8; ++e) f[e] = 0.f;
         float lo = f[0], hi = f[0];
 #pragma unroll
-        for (int e = 1; e < 32; ++e) { lo = fminf(lo, f[e]); hi = fmaxf(hi, f[e]); }
+        for (int e = 1; e < 8; ++e) { lo = fminf(lo, f[e]); hi = fmaxf(hi, f[e]); }
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 1)); hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, 1));
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 2)); hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, 2));
+        if (!ok) continue;
         const __nv_bfloat16 zb = __float2bfloat16_rn(lo);
         const __nv_bfloat16 sb = __float2bfloat16_rn(__fdiv_rn(hi - lo, (float)qmax));
         const float zf = __bfloat162float(zb), sf = __bfloat162float(sb);
+        const float inv = sf > 0.f ? __frcp_rn(sf) : 0.f;
+        uint32_t w = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int c = min(qmax, max(0, __float2int_rn((f[e] - zf) * inv)));
+          w |= (uint32_t)c << (e * bits);
+        }
         const int pb = a.pos ? a.pos[b] : a.seq_len[b] - 1;
         char* row = reinterpret_cast<char*>(a.v_cache) + ((size_t)b * a.cap + pb) * a.v_row_bytes + (size_t)h * hb;
-        uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          int c = 0;
-          if (sf > 0.f) c = min(qmax, max(0, __float2int_rn(__fdiv_rn(f[e] - zf, sf))));
-          const int bitpos = e * bits;
-          w[bitpos >> 5] |= (uint32_t)c << (bitpos & 31);
-        }
-        if (bits == 4) *reinterpret_cast<uint4*>(row + gq * 16) = make_uint4(w[0], w[1], w[2], w[3]);
-        else *reinterpret_cast<uint2*>(row + gq * 8) = make_uint2(w[0], w[1]);
-        const uint32_t par = (uint32_t)__bfloat16_as_ushort(sb) | ((uint32_t)__bfloat16_as_ushort(zb) << 16);
-        *reinterpret_cast<uint32_t*>(row + 128 * bits / 8 + gq * 4) = par;
+        if (bits == 4) *reinterpret_cast<uint32_t*>(row + gq * 16 + q * 4) = w;
+        else *reinterpret_cast<uint16_t*>(row + gq * 8 + q * 2) = (uint16_t)w;
+        if (q == 0)
+          *reinterpret_cast<uint32_t*>(row + 128 * bits / 8 + gq * 4) =
+              (uint32_t)__bfloat16_as_ushort(sb) | ((uint32_t)__bfloat16_as_ushort(zb) << 16);
       }
     }
   }
