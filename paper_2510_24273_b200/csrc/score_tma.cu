@@ -105,11 +105,15 @@ score_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant_
     // ================= producer: one TMA box per (request, 32-token chunk) =================
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(&map) : "memory");
-      if (a.stream_after_wait) pdl_wait();   // new latent rows written by the kernel just before
+      // stream_after_wait: the new token's latent row (slot len - 1) was written by the
+      // kernel just before (fused append): the chunk holding it is loaded only after
+      // griddepcontrol.wait; every older row streams before it
+      bool waited = !a.stream_after_wait;
       int u = 0, b = i0 / nchunk, c = i0 - b * nchunk;
       int len = i0 < i1 ? a.len[b] : 0;
       for (int it = i0; it < i1; ++it) {
         if (c * kTok < len) {
+          if (!waited && (c + 1) * kTok >= len) { pdl_wait(); waited = true; }
           const int s = u % kStages;
           if (u >= kStages) mbar_wait(&empty[s], ((u / kStages) - 1) & 1);
           mbar_arrive_expect_tx(&full[s], (uint32_t)stage_bytes);
