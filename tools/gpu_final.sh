@@ -6,3 +6,4 @@ bash tools/gpu_round.sh $tag
 timeout 600 python bench.py --workload c4-sharded --steps 20 --warmup 5 > gpurun_out/bench_${tag}_c4sharded.json 2> gpurun_out/bench_${tag}_c4sharded.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_${tag}_reference.json 2> gpurun_out/bench_${tag}_reference.err
 bash tools/gpu_ncu.sh $tag c2 "project score_tma topk recon_attn"
+bash tools/gpu_sweep.sh $tag
