@@ -273,11 +273,17 @@ def run_sals(args, rank, world):
     if args.v_bits:   # quantised value rows (synthetic codes, valid bf16 scale / zero per group)
         rb = sals.sals_v_row_bytes(cfg)
         nbc = sh["head_dim"] * args.v_bits // 8
+        z = pol["recent"]
+        par = torch.tensor([0.05, -0.4], dtype=torch.bfloat16, device=dev).view(torch.uint8).repeat(4)
+        par8 = torch.tensor([0.003, -0.4], dtype=torch.bfloat16, device=dev).view(torch.uint8).repeat(4)
         for ly in layers:
-            vq = torch.randint(0, 256, (B, s, sh["num_kv_heads"], nbc + 16), dtype=torch.uint8, device=dev)
-            par = torch.tensor([0.05, -0.4], dtype=torch.bfloat16, device=dev).view(torch.uint8)
-            vq[..., nbc:] = par.repeat(4)
-            ly["vq"] = vq.view(B, s, rb)
+            buf = torch.randint(0, 256, (sals.sals_v_cache_bytes(cfg, B, s),), dtype=torch.uint8, device=dev)
+            main = buf[:B * s * rb].view(B, s, sh["num_kv_heads"], nbc + 16)
+            main[..., nbc:] = par
+            if z:   # the 8-bit recent-window ring after the rows
+                ring = buf[B * s * rb:].view(B, z, sh["num_kv_heads"], 144)
+                ring[..., 128:] = par8
+            ly["vq"] = buf
     vkey = "vq" if args.v_bits else "v"
     D, nqd = sh["num_kv_heads"] * sh["head_dim"], sh["num_q_heads"] * sh["head_dim"]
     seq = torch.full((B,), s, dtype=torch.int32, device=dev)

@@ -79,6 +79,14 @@ typedef struct {
 /* Bytes of one token's row of the value cache (D * sizeof(dtype), or the
  * quantised layout above).  0 on invalid arguments. */
 size_t sals_v_row_bytes(const sals_config* cfg);
+/* Bytes of a value cache of `batch` requests x `cap` rows.  With v_bits 4 / 2
+ * and recent = w > 0 the high-precision recent window ("tokens in the
+ * most recent window are compressed by only 50%", aligned with the forced recent
+ * window of the selection) follows the rows: a ring [batch, w, n_kv * 144] of
+ * 8-bit rows (128 code bytes + 4 (bf16 scale, bf16 zero) per head), slot
+ * pos % w; the decode reads positions >= s_b - w from it.  Not with the sharded
+ * calls. */
+size_t sals_v_cache_bytes(const sals_config* cfg, int32_t batch, int64_t cap);
 
 /* Bytes of device workspace sals_decode needs for `batch` requests of at most
  * `max_seq_len` tokens.  0 on invalid arguments. */

@@ -90,6 +90,9 @@ int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 // quantised value cache: bits per value (0 = dtype values)
 inline int vq_bits(const sals_config* c) { return (c->v_bits == 4 || c->v_bits == 2) ? c->v_bits : 0; }
+// high-precision recent window of the quantised value cache (8-bit ring of cfg->recent rows)
+inline int hp_window(const sals_config* c) { return vq_bits(c) ? c->recent : 0; }
+inline size_t hp_row_bytes(const sals_config* c) { return (size_t)c->num_kv_heads * (128 + 16); }
 inline size_t v_row_bytes(const sals_config* c) {
   const int d = c->head_dim, nkv = c->num_kv_heads;
   if (vq_bits(c)) return (size_t)nkv * ((size_t)d * c->v_bits / 8 + (size_t)(d / 32) * 4);
@@ -421,13 +424,16 @@ sals_status launch_merge(const sals_config* c, MergeArgs a, int batch, cudaStrea
 template <typename T>
 sals_status attend_list(const sals_config* c, const Plan& p, const void* U, const void* latent,
                         const void* v_cache, int64_t cap, int batch, int64_t pos_base, const int* sel,
-                        const int* count, char* ws, void* out, float* partial_out, cudaStream_t st) {
+                        const int* count, char* ws, void* out, float* partial_out, cudaStream_t st,
+                        const int* seq_len_hp = nullptr) {
   float* part = reinterpret_cast<float*>(ws + p.off_part);
   const float* qrope = reinterpret_cast<const float*>(ws + p.off_qrope);
   if (p.tc) {
     TcArgs t{};
     t.latent = latent; t.cap = cap; t.r = c->rank; t.U = U; t.v_cache = v_cache;
     t.v_bits = vq_bits(c); t.v_row_bytes = (int)v_row_bytes(c);
+    t.hp_window = seq_len_hp ? hp_window(c) : 0;
+    t.hp_ring_off = (int64_t)batch * cap * (int64_t)v_row_bytes(c); t.seq_len = seq_len_hp;
     t.sel = sel; t.count = count; t.k_stride = c->top_k; t.D = p.D; t.head_dim = c->head_dim;
     t.G = p.G; t.n_q = c->num_q_heads; t.pos_base = pos_base; t.rope = make_rope(c);
     t.qrope = qrope; t.scale_log2 = scale_log2(c); t.partials = part; t.ntiles = p.nsplit;
@@ -502,6 +508,7 @@ sals_status decode_impl(const sals_config* c, const void* U, const void* q, cons
   if (fused) {
     pa.xa = k_new; pa.ncols_a = c->rank; pa.v_new = v_new; pa.pos = nullptr;
     pa.v_bits = vq_bits(c); pa.v_row_bytes = (int)v_row_bytes(c);
+    pa.hp_window = hp_window(c); pa.hp_ring_off = (int64_t)batch * cap * (int64_t)v_row_bytes(c);
     pa.latent = const_cast<void*>(latent); pa.v_cache = const_cast<void*>(v_cache); pa.cap = cap;
     Plan pf = p;
     plan_proj(pf, false);   // the append's cluster shape (more column blocks)
@@ -531,7 +538,7 @@ sals_status decode_impl(const sals_config* c, const void* U, const void* q, cons
   if (s != SALS_OK) return s;
   mark(kStTopk, st);
 
-  return attend_list<T>(c, p, U, latent, v_cache, cap, batch, 0, sel, count, ws, out, nullptr, st);
+  return attend_list<T>(c, p, U, latent, v_cache, cap, batch, 0, sel, count, ws, out, nullptr, st, seq_len);
 }
 
 }  // namespace
@@ -555,6 +562,11 @@ const char* sals_last_error(void) { return g_err.c_str(); }
 size_t sals_v_row_bytes(const sals_config* cfg) {
   if (validate(cfg) != SALS_OK) return 0;
   return v_row_bytes(cfg);
+}
+
+size_t sals_v_cache_bytes(const sals_config* cfg, int32_t batch, int64_t cap) {
+  if (validate(cfg) != SALS_OK || batch < 1 || cap < 1) return 0;
+  return (size_t)batch * cap * v_row_bytes(cfg) + (size_t)batch * hp_window(cfg) * hp_row_bytes(cfg);
 }
 
 uint32_t sals_profile_stage_mask(uint32_t mask) {
@@ -590,6 +602,7 @@ sals_status sals_append_latent(const sals_config* cfg, const void* U, const void
   a.head_dim = cfg->head_dim; a.group = 1; a.n_q = cfg->num_q_heads; a.latent = latent_cache; a.cap = cap;
   a.pos = d_pos; a.v_new = v_new; a.v_cache = v_cache;
   a.v_bits = vq_bits(cfg); a.v_row_bytes = (int)v_row_bytes(cfg);
+  a.hp_window = hp_window(cfg); a.hp_ring_off = (int64_t)batch * cap * (int64_t)v_row_bytes(cfg);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (!on(kNumStages)) return SALS_OK;
   if (cfg->dtype == SALS_BF16) return launch_project<__nv_bfloat16>(cfg, p, 0, a, st);
@@ -879,6 +892,7 @@ sals_status sals_shard_attend(const sals_config* cfg, const void* U, const void*
   oa.gsel = gsel; oa.gcount = gcount; oa.g_stride = cfg->top_k; oa.seq_len = d_seq_len; oa.local_len = d_local_len;
   oa.shard_start = shard_start; oa.sink = cfg->sink; oa.recent = cfg->recent; oa.k = cfg->top_k;
   oa.own_sel = own; oa.own_count = own_count;
+  if (hp_window(cfg)) return fail(SALS_ERR_UNSUPPORTED, "the quantised values' recent window is not sharded");
   SALS_CUDA_TRY(launch(owned_list_kernel, dim3(batch), dim3(256), 0, st, 0, oa));
   if (cfg->dtype == SALS_BF16)
     return attend_list<__nv_bfloat16>(cfg, p, U, latent_shard, v_shard, cap_local, batch, shard_start, own,

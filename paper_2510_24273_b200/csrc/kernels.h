@@ -39,6 +39,8 @@ struct ProjectArgs {
   // pos == nullptr -> the new token's slot is seq_len[b] - 1
   const void* xa; int ncols_a; int n_append_blocks;
   int v_bits, v_row_bytes;   // value row format (0: dtype values; 4 / 2: quantised, head_dim 128)
+  int hp_window;             // > 0: the last hp_window tokens also kept at 8 bits in a ring after the main rows
+  int64_t hp_ring_off;       // bytes from v_cache to the ring [B, hp_window, n_kv * 144]
 };
 
 struct ScoreArgs {

@@ -171,6 +171,23 @@ project_kernel(ProjectArgs a) {
         if (q == 0)
           *reinterpret_cast<uint32_t*>(row + 128 * bits / 8 + gq * 4) =
               (uint32_t)__bfloat16_as_ushort(sb) | ((uint32_t)__bfloat16_as_ushort(zb) << 16);
+        if (a.hp_window > 0) {
+          // high-precision copy of the recent window: 8 bits in ring slot pos % w
+          const __nv_bfloat16 s8 = __float2bfloat16_rn(__fdiv_rn(hi - lo, 255.f));
+          const float s8f = __bfloat162float(s8), inv8 = s8f > 0.f ? __frcp_rn(s8f) : 0.f;
+          uint32_t w8[2] = {0, 0};
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int c = min(255, max(0, __float2int_rn((f[e] - zf) * inv8)));
+            w8[e >> 2] |= (uint32_t)c << ((e & 3) * 8);
+          }
+          char* ring = reinterpret_cast<char*>(a.v_cache) + a.hp_ring_off +
+                       ((size_t)b * a.hp_window + pb % a.hp_window) * (size_t)(a.D / 128) * 144 + (size_t)h * 144;
+          *reinterpret_cast<uint2*>(ring + gq * 32 + q * 8) = make_uint2(w8[0], w8[1]);
+          if (q == 0)
+            *reinterpret_cast<uint32_t*>(ring + 128 + gq * 4) =
+                (uint32_t)__bfloat16_as_ushort(s8) | ((uint32_t)__bfloat16_as_ushort(zb) << 16);
+        }
       }
     }
   }

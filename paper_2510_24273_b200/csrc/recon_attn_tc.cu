@@ -416,7 +416,7 @@ cudaError_t launch_g(const CUtensorMap& map, const TcArgs& a, int batch, cudaStr
 }  // namespace
 
 cudaError_t launch_recon_attn_tc2(const CUtensorMap& map, const CUtensorMap& ml, const CUtensorMap& mv,
-                                  const TcArgs& a, int batch, cudaStream_t st);
+                                  const CUtensorMap& mvh, const TcArgs& a, int batch, cudaStream_t st);
 
 bool tc_supported(int head_dim, int D, int rank, int G) {
   return (head_dim == 64 || head_dim == 128 || head_dim == 256) && D % kBN == 0 && rank % kBK == 0 &&
@@ -466,7 +466,21 @@ sals_status launch_recon_attn_tc(const TcArgs& a, int batch, cudaStream_t st) {
       g_tc_err = "cuTensorMapEncodeTiled failed for the gather maps";
       return SALS_ERR_CUDA;
     }
-    e = launch_recon_attn_tc2(map, ml, mv, a, batch, st);
+    // (quantised values) the 8-bit recent-window ring [B * w, n_kv * 144] after the rows
+    CUtensorMap mvh = mv;
+    if (vq && a.hp_window > 0) {
+      const cuuint64_t hrow = (cuuint64_t)(a.D / 128) * 144;
+      cuuint64_t dh[2] = {hrow, (cuuint64_t)batch * (cuuint64_t)a.hp_window}, sh[1] = {hrow};
+      cuuint32_t bh[2] = {144u, 1};   // one KV head per box (boxes are <= 256 elements)
+      if (g_encode(&mvh, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2,
+                   const_cast<char*>(reinterpret_cast<const char*>(a.v_cache)) + a.hp_ring_off, dh, sh, bh, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+        g_tc_err = "cuTensorMapEncodeTiled failed for the recent-window map";
+        return SALS_ERR_CUDA;
+      }
+    }
+    e = launch_recon_attn_tc2(map, ml, mv, mvh, a, batch, st);
     if (e != cudaSuccess) { g_tc_err = cudaGetErrorString(e); return SALS_ERR_CUDA; }
     return SALS_OK;
   }

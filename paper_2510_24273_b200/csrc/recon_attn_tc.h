@@ -26,6 +26,9 @@ struct TcArgs {
   unsigned* counters;     // v2, nullable: [B, D/256] arrival counters, zero on entry
   int v_bits;             // 0: dtype values; 4 / 2: quantised value rows (v2 only)
   int v_row_bytes;        // bytes of one token's value row
+  int hp_window;          // > 0: positions >= s_b - hp_window read their 8-bit ring rows (DESIGN R15)
+  int64_t hp_ring_off;    // bytes from v_cache to the ring [B, hp_window, n_kv * 144]
+  const int* seq_len;     // [B] (hp window)
 };
 
 bool tc_supported(int head_dim, int D, int rank, int G);

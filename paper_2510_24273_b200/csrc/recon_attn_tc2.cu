@@ -227,10 +227,14 @@ __device__ unsigned long long g_trace[128];
 template <int G, int STYLE, int VB>
 __global__ void __launch_bounds__(kThreads, 1)
 recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_constant__ CUtensorMap tmap_lat,
-                      const __grid_constant__ CUtensorMap tmap_v, const __grid_constant__ KArgs ka) {
+                      const __grid_constant__ CUtensorMap tmap_v, const __grid_constant__ CUtensorMap tmap_vh,
+                      const __grid_constant__ KArgs ka) {
   constexpr int NQH = 2 * G;             // query heads of this CTA (2 KV heads)
   constexpr int kVHead = VB == 16 ? kDH * 2 : kDH * VB / 8 + (kDH / 32) * 4;   // value bytes per head-token
   constexpr int kVRow = 2 * kVHead;                                           // bytes of a V tile row (2 heads)
+  constexpr int kVRowH = 2 * 144;   // (quantised) 8-bit recent-window row of the 2 heads (DESIGN R15)
+  constexpr int kHGrp = 1280;       // smem of 4 such rows: [4 x 144 B head 0 | pad to 640 | 4 x 144 B head 1 | pad]
+                                    // (TMA destinations 128-B aligned)
   const TcArgs& a = ka.a;
   extern __shared__ uint8_t smem_raw[];
   // align with pointer arithmetic on the __shared__ array so the compiler keeps the shared
@@ -253,6 +257,9 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
   uint64_t* vfull = tempty + 2;
   uint64_t* vempty = vfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(vempty + 1);
+  int* s_thp = reinterpret_cast<int*>(tmem_slot + 1);   // first tile token read from the 8-bit recent window
+  uint8_t* sVh = sV + kRows * kVRow;                      // (quantised) 8-bit rows of the recent window
+  static_assert(VB == 16 || kRows * kVRow + 32 * 1280 <= kVBytes, "recent-window staging exceeds the V tile");
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int chunk = blockIdx.x, nb = blockIdx.y, b = blockIdx.z;
@@ -369,10 +376,41 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
         idx[t] = t < nv ? b * (int)a.cap + selb[tile * kRows + t] : -1;
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive_expect_tx(vfull, (uint32_t)(kRows * kVRow));
+      // quantised values with a recent window: tokens at positions >= s_b - w (a suffix of
+      // the ascending tile) are read from the 8-bit ring (slot pos % w) into sVh
+      int thp = nv;
+      if constexpr (VB != 16) {
+        if (a.hp_window > 0) {
+          const int lim = a.seq_len[b] - a.hp_window;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int t = lane + 32 * j;
+            if (t < nv && selb[tile * kRows + t] >= lim) thp = min(thp, t);
+          }
+          thp = __reduce_min_sync(0xffffffffu, thp);
+        }
+      }
+      const bool hp_lane = VB != 16 && thp < nv && 4 * lane + 3 >= thp && 4 * lane < nv;
+      const int n_hp = __popc(__ballot_sync(0xffffffffu, hp_lane));
+      if (lane == 0) {
+        *s_thp = thp;
+        mbar_arrive_expect_tx(vfull, (uint32_t)(kRows * kVRow + n_hp * 4 * kVRowH));
+      }
       __syncwarp();
       tma_gather4(smem_u32(sV + lane * 4 * kVRow), &tmap_v, VB == 16 ? n0 : nb * kVRow, idx[4 * lane], idx[4 * lane + 1],
                   idx[4 * lane + 2], idx[4 * lane + 3], vfull);
+      if (hp_lane) {
+        int ri[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int t = 4 * lane + e;
+          ri[e] = (t >= thp && t < nv) ? b * a.hp_window + selb[tile * kRows + t] % a.hp_window : -1;
+        }
+        // box rows are <= 256 bytes: one gather per KV head (4 rows x 144 B each)
+        tma_gather4(smem_u32(sVh + lane * kHGrp), &tmap_vh, nb * kVRowH, ri[0], ri[1], ri[2], ri[3], vfull);
+        tma_gather4(smem_u32(sVh + lane * kHGrp + kHGrp / 2), &tmap_vh, nb * kVRowH + 144, ri[0], ri[1], ri[2],
+                    ri[3], vfull);
+      }
       if (it + 1 < ntile) {   // next tile's V rows -> L2 via the LSU (keeps the TMA queue for loads)
         const int ntl = tile + 1;
         const int nnv = min(kRows, cnt - ntl * kRows);
@@ -556,6 +594,7 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
         }
         const uint4* vrow = reinterpret_cast<const uint4*>(sV) + lane;   // (VB 16) row t at vrow[t * 32]
         const uint8_t* qrow = sV + kh * kVHead;                            // (quantised) row t at qrow[t * kVRow]
+        const int thp = *s_thp;                                            // tokens >= thp: 8-bit window rows
         const float* pp = sP + kh * G * kPS;
         const int tb = 16 * ew;
 #pragma unroll
@@ -574,6 +613,19 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
                 const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
                 for (int e = 0; e < 4; ++e) vv[e] = make_float2(__uint_as_float(w[e] << 16), __uint_as_float(w[e] & 0xffff0000u));
+              } else if (t0 + j >= thp) {   // 8-bit recent-window row
+                // group of 4 tokens: [4 x 144 B of head 0 | pad][4 x 144 B of head 1 | pad]
+                const int tt = t0 + j;
+                const uint8_t* rh = sVh + (tt >> 2) * kHGrp + kh * (kHGrp / 2) + (tt & 3) * 144;
+                const int l8 = lane & 15;
+                const uint32_t par = *reinterpret_cast<const uint32_t*>(rh + 128 + 4 * (l8 >> 2));
+                const float sf = __uint_as_float(par << 16), zf = __uint_as_float(par & 0xffff0000u);
+                const uint2 cw = *reinterpret_cast<const uint2*>(rh + 8 * l8);
+                const uint32_t w2[2] = {cw.x, cw.y};
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  vv[e] = make_float2(fmaf(sf, (float)((w2[e >> 1] >> (16 * (e & 1))) & 255u), zf),
+                                      fmaf(sf, (float)((w2[e >> 1] >> (16 * (e & 1) + 8)) & 255u), zf));
               } else {
                 const uint8_t* rq = qrow + (t0 + j) * kVRow;
                 const int l8 = lane & 15;
@@ -659,8 +711,8 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
 }
 
 template <int G, int STYLE, int VB>
-cudaError_t launch_t(const CUtensorMap& map, const CUtensorMap& map_lat, const CUtensorMap& map_v, const TcArgs& a,
-                     int batch, cudaStream_t st) {
+cudaError_t launch_t(const CUtensorMap& map, const CUtensorMap& map_lat, const CUtensorMap& map_v,
+                     const CUtensorMap& map_vh, const TcArgs& a, int batch, cudaStream_t st) {
   auto kern = recon_attn_tc2_kernel<G, STYLE, VB>;
   static bool attr = false;
   if (!attr) {
@@ -679,7 +731,7 @@ cudaError_t launch_t(const CUtensorMap& map, const CUtensorMap& map_lat, const C
   cfg.attrs = at;
   cfg.numAttrs = 1;
   KArgs ka{a};
-  return cudaLaunchKernelEx(&cfg, kern, map, map_lat, map_v, ka);
+  return cudaLaunchKernelEx(&cfg, kern, map, map_lat, map_v, map_vh, ka);
 }
 
 }  // namespace tc2
@@ -703,13 +755,13 @@ bool tc2_supported(int head_dim, int D, int rank, int G) {
 }
 
 cudaError_t launch_recon_attn_tc2(const CUtensorMap& map, const CUtensorMap& ml, const CUtensorMap& mv,
-                                  const TcArgs& a, int batch, cudaStream_t st) {
+                                  const CUtensorMap& mvh, const TcArgs& a, int batch, cudaStream_t st) {
   const int style = a.rope.style;
 #define SALS_TC2_VB(VB)                                                                                         \
   switch (a.G) {                                                                                                \
-    case 1: return style ? tc2::launch_t<1, 1, VB>(map, ml, mv, a, batch, st) : tc2::launch_t<1, 0, VB>(map, ml, mv, a, batch, st); \
-    case 2: return style ? tc2::launch_t<2, 1, VB>(map, ml, mv, a, batch, st) : tc2::launch_t<2, 0, VB>(map, ml, mv, a, batch, st); \
-    case 4: return style ? tc2::launch_t<4, 1, VB>(map, ml, mv, a, batch, st) : tc2::launch_t<4, 0, VB>(map, ml, mv, a, batch, st); \
+    case 1: return style ? tc2::launch_t<1, 1, VB>(map, ml, mv, mvh, a, batch, st) : tc2::launch_t<1, 0, VB>(map, ml, mv, mvh, a, batch, st); \
+    case 2: return style ? tc2::launch_t<2, 1, VB>(map, ml, mv, mvh, a, batch, st) : tc2::launch_t<2, 0, VB>(map, ml, mv, mvh, a, batch, st); \
+    case 4: return style ? tc2::launch_t<4, 1, VB>(map, ml, mv, mvh, a, batch, st) : tc2::launch_t<4, 0, VB>(map, ml, mv, mvh, a, batch, st); \
   }                                                                                                             \
   return cudaErrorInvalidValue;
   if (a.v_bits == 4) { SALS_TC2_VB(4) }

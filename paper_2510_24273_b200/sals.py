@@ -25,7 +25,7 @@ EXPORTED = ["sals_workspace_bytes", "sals_append_latent", "sals_decode", "sals_d
             "sals_merge_partials", "sals_shard_workspace_bytes", "sals_status_string", "sals_last_error",
             "sals_launch_count", "sals_profile_stage_mask", "sals_append_decode",
             "sals_append_latent_bulk", "sals_calibrate_workspace_bytes", "sals_calibrate",
-            "sals_v_row_bytes"]
+            "sals_v_row_bytes", "sals_v_cache_bytes"]
 
 
 class SalsError(RuntimeError):
@@ -69,6 +69,7 @@ def _load():
         "sals_append_latent_bulk": (I32, [C, P, P, P, I32, I32, I64, P, P, I64, P]),
         "sals_calibrate_workspace_bytes": (SZ, [C]),
         "sals_v_row_bytes": (SZ, [C]),
+        "sals_v_cache_bytes": (SZ, [C, I32, I64]),
         "sals_calibrate": (I32, [C, P, I64, P, P, P, SZ, P]),
         "sals_decode_profile": (I32, [C, P, P, P, P, I64, I32, P, I32, P, P, SZ, I32, P, P]),
         "sals_dense_append": (I32, [C, P, P, I32, P, P, P, I64, P]),
@@ -142,6 +143,11 @@ STAGES = ["qproj_rope", "score", "topk", "recon_attn", "flash", "merge"]
 def sals_v_row_bytes(cfg) -> int:
     """Bytes of one token's value-cache row (D * dtype size, or the quantised layout of cfg.v_bits)."""
     return int(_lib.sals_v_row_bytes(ctypes.byref(cfg)))
+
+
+def sals_v_cache_bytes(cfg, batch: int, cap: int) -> int:
+    """Bytes of a value cache (rows + the quantised values' 8-bit recent-window ring)."""
+    return int(_lib.sals_v_cache_bytes(ctypes.byref(cfg), int(batch), int(cap)))
 
 
 def sals_calibrate_workspace_bytes(cfg) -> int:

@@ -432,3 +432,79 @@ def test_quantized_values_decode(bits, nkv, G):
         forced.append(srow[srow >= 0].astype(np.int64))
     orc_f = O.decode(oc, H.widen(U), H.widen(q), host_lat, vhat, np.array(seqs), forced_selection=forced)
     H.check_output(H.widen(out), orc_f["y"], "bf16")
+
+
+def _pack8(v, nkv):
+    """8-bit rows of the recent-window ring: per KV head 128 code bytes + 4 (bf16 scale, bf16 zero)."""
+    codes, scale, zero = O.quantize_values(v, 8, 32)
+    lead = v.shape[:-1]
+    c = codes.reshape(*lead, nkv, 128).astype(np.uint8)
+    sb = torch.from_numpy(scale.astype(np.float32)).bfloat16().view(torch.int16).numpy().view(np.uint16)
+    zb = torch.from_numpy(zero.astype(np.float32)).bfloat16().view(torch.int16).numpy().view(np.uint16)
+    par = np.stack([sb, zb], -1).reshape(*lead, nkv, 4, 2).view(np.uint8).reshape(*lead, nkv, 16)
+    return np.concatenate([c, par], -1).reshape(*lead, -1)
+
+
+def _unpack8(rows, nkv):
+    lead = rows.shape[:-1]
+    r = rows.reshape(*lead, nkv, 144)
+    codes = r[..., :128].astype(np.int64).reshape(*lead, nkv * 128)
+    par = np.ascontiguousarray(r[..., 128:]).view(np.uint16).reshape(*lead, nkv, 4, 2)
+    to_f = lambda u: torch.from_numpy(u.astype(np.int16)).view(torch.bfloat16).float().numpy().astype(np.float64)
+    return O.dequantize_values(codes, to_f(par[..., 0]).reshape(*lead, -1), to_f(par[..., 1]).reshape(*lead, -1), 32)
+
+
+@pytest.mark.parametrize("bits,nkv,G,z", [(4, 8, 4, 64), (2, 4, 1, 100)])
+def test_quantized_values_recent_window(bits, nkv, G, z):
+    """Quantised values with the high-precision recent window: the forced
+    recent z tokens are read from the 8-bit ring, the rest from the b-bit rows; the
+    append writes both formats.  Checked against the oracle over the stored V^."""
+    from paper_2510_24273_b200 import sals
+    d, B, seqs, k = 128, 2, [3000, 2311], 384
+    sh = dict(num_q_heads=nkv * G, num_kv_heads=nkv, head_dim=d, rank=256, score_rank=128, top_k=k,
+              rope_base=1e6, dtype="bf16")
+    cfg = sals.make_config(**sh, v_bits=bits, recent=z)
+    p = synth.gen_problem(num_q_heads=nkv * G, num_kv_heads=nkv, head_dim=d, rank=256, batch=B, seq_lens=seqs, seed=23)
+    cap = max(seqs)
+    dev = lambda a: torch.from_numpy(a).cuda().bfloat16()
+    U, q, kn, vn, lat = dev(p["U"]), dev(p["q"]), dev(p["k_new"]), dev(p["v_new"]), dev(p["latent"])
+    v_host = H.widen(dev(p["v"]))
+    rb = sals.sals_v_row_bytes(cfg)
+    total = sals.sals_v_cache_bytes(cfg, B, cap)
+    assert total == B * cap * rb + B * z * nkv * 144
+    main = _pack_values(v_host, bits, nkv)                               # [B, cap, rb]
+    ring = np.zeros((B, z, nkv * 144), dtype=np.uint8)
+    for b in range(B):
+        for pos in range(seqs[b] - z, seqs[b]):
+            ring[b, pos % z] = _pack8(v_host[b, pos][None], nkv)[0]
+    vq = torch.from_numpy(np.concatenate([main.reshape(-1), ring.reshape(-1)])).cuda()
+    seq = torch.tensor(seqs, dtype=torch.int32, device="cuda")
+    ws = sals.alloc_workspace(sals.sals_workspace_bytes(cfg, B, cap), "cuda")
+    out = torch.empty(B, nkv * G * d, dtype=torch.bfloat16, device="cuda")
+    sel = torch.full((B, k), -7, dtype=torch.int32, device="cuda")
+    sals.sals_append_decode(cfg, U, kn, vn, q, lat, vq, seq, cap, out, ws, sel_idx_out=sel)
+    torch.cuda.synchronize()
+    allb = vq.cpu().numpy()
+    rows = allb[:B * cap * rb].reshape(B, cap, rb)
+    ringg = allb[B * cap * rb:].reshape(B, z, nkv * 144)
+    vhat = _unpack_values(rows, bits, nkv)
+    for b in range(B):
+        s = seqs[b]
+        # the append's 8-bit row of the new token vs the oracle quantiser (one code step)
+        _, sc8, _ = O.quantize_values(H.widen(vn[b:b + 1]), 8, 32)
+        got8 = _unpack8(ringg[b, (s - 1) % z][None], nkv)[0]
+        ref8 = _unpack8(_pack8(H.widen(vn[b:b + 1]), nkv), nkv)[0]
+        assert np.all(np.abs(got8 - ref8) <= sc8.repeat(32, -1)[0] * 1.01 + 1e-6)
+        for pos in range(s - z, s):
+            vhat[b, pos] = _unpack8(ringg[b, pos % z][None], nkv)[0]
+    oc = H.oracle_cfg(sh, recent=z)
+    host_lat = H.widen(lat)
+    orc = O.decode(oc, H.widen(U), H.widen(q), host_lat, vhat, np.array(seqs))
+    forced = []
+    for b in range(B):
+        srow = sel.cpu().numpy()[b]
+        H.check_selection(orc["scores"][b], orc["sel"][b], srow, seqs[b], k, 0, z)
+        assert np.all(np.isin(np.arange(seqs[b] - z, seqs[b]), srow))
+        forced.append(srow[srow >= 0].astype(np.int64))
+    orc_f = O.decode(oc, H.widen(U), H.widen(q), host_lat, vhat, np.array(seqs), forced_selection=forced)
+    H.check_output(H.widen(out), orc_f["y"], "bf16")
