@@ -366,6 +366,7 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
     // warms L2 with the next tile's V and latent rows ========
     const char* vb = reinterpret_cast<const char*>(a.v_cache);
     int* idx = sIdxV;
+    const int hp_lim = (VB != 16 && a.hp_window > 0) ? max(0, a.seq_len[b] - a.hp_window) : -1;
     for (int it = 0; it < ntile; ++it) {
       const int tile = t_begin + it;
       const int nv = min(kRows, cnt - tile * kRows);
@@ -380,12 +381,11 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
       // the ascending tile) are read from the 8-bit ring (slot pos % w) into sVh
       int thp = nv;
       if constexpr (VB != 16) {
-        if (a.hp_window > 0) {
-          const int lim = a.seq_len[b] - a.hp_window;
+        if (hp_lim >= 0) {   // positions from the indices just staged (no second global read)
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const int t = lane + 32 * j;
-            if (t < nv && selb[tile * kRows + t] >= lim) thp = min(thp, t);
+            if (t < nv && idx[t] - b * (int)a.cap >= hp_lim) thp = min(thp, t);
           }
           thp = __reduce_min_sync(0xffffffffu, thp);
         }
@@ -404,7 +404,7 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int t = 4 * lane + e;
-          ri[e] = (t >= thp && t < nv) ? b * a.hp_window + selb[tile * kRows + t] % a.hp_window : -1;
+          ri[e] = (t >= thp && t < nv) ? b * a.hp_window + (idx[t] - b * (int)a.cap) % a.hp_window : -1;
         }
         // box rows are <= 256 bytes: one gather per KV head (4 rows x 144 B each)
         tma_gather4(smem_u32(sVh + lane * kHGrp), &tmap_vh, nb * kVRowH, ri[0], ri[1], ri[2], ri[3], vfull);
