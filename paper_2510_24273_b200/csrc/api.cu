@@ -221,13 +221,13 @@ int flash_tpw_unr(const sals_config* c) {
 }
 
 // Rows of U per CTA of the projection cluster: a multiple of 8 (16-byte vectors),
-// at most 512.  Measured (bench stage times, c2 D = 4096 / c3 D = 1024): 8-CTA
-// clusters for the append (8 column blocks at r = 512) and for D <= 2048; the
-// query projection at D = 4096 (4 column blocks at r* = 256) prefers 16 (all
-// 256 rows of a CTA prefetched before the PDL wait).
+// at most 512 (the CTA's U slice, rows x 128 B, is staged in shared memory
+// before the PDL wait).  Measured (bench stage times, c2 D = 4096 / c3 D = 1024):
+// 8-CTA clusters beat 16 (a 16-CTA cluster needs 16 free SMs of one GPC) and 4.
 void plan_proj(Plan& p, bool query) {
+  (void)query;
   static const int cs_env = [] { const char* e = getenv("SALS_PROJ_CS"); return e ? atoi(e) : 0; }();
-  int cs = std::min((query && p.D > 2048) ? 16 : 8, std::max(1, ceil_div(p.D, 64)));
+  int cs = std::min(8, std::max(1, ceil_div(p.D, 64)));
   while (ceil_div(p.D, cs) > 512) cs *= 2;
   if (cs_env >= 1 && cs_env <= 16 && ceil_div(p.D, cs_env) <= 512) cs = cs_env;   // experiment override
   p.proj_rows = (int)align_up(ceil_div(p.D, cs), 8);
@@ -293,11 +293,15 @@ sals_status launch_project(const sals_config* c, const Plan& p, int mode, Projec
     SALS_CUDA_TRY(cudaFuncSetAttribute(project_kernel<T, 0>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     SALS_CUDA_TRY(cudaFuncSetAttribute(project_kernel<T, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     SALS_CUDA_TRY(cudaFuncSetAttribute(project_kernel<T, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    SALS_CUDA_TRY(cudaFuncSetAttribute(project_kernel<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    SALS_CUDA_TRY(cudaFuncSetAttribute(project_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    SALS_CUDA_TRY(cudaFuncSetAttribute(project_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     attr_done = true;
   }
-  if (mode == 0) SALS_CUDA_TRY(launch(project_kernel<T, 0>, grid, dim3(kProjThreads), 0, st, p.proj_cs, a));
-  else if (mode == 1) SALS_CUDA_TRY(launch(project_kernel<T, 1>, grid, dim3(kProjThreads), 0, st, p.proj_cs, a));
-  else SALS_CUDA_TRY(launch(project_kernel<T, 2>, grid, dim3(kProjThreads), 0, st, p.proj_cs, a));
+  const size_t smem = (size_t)p.proj_rows * 128;   // the CTA's U slice (rows x 128 B)
+  if (mode == 0) SALS_CUDA_TRY(launch(project_kernel<T, 0>, grid, dim3(kProjThreads), smem, st, p.proj_cs, a));
+  else if (mode == 1) SALS_CUDA_TRY(launch(project_kernel<T, 1>, grid, dim3(kProjThreads), smem, st, p.proj_cs, a));
+  else SALS_CUDA_TRY(launch(project_kernel<T, 2>, grid, dim3(kProjThreads), smem, st, p.proj_cs, a));
   return SALS_OK;
 }
 

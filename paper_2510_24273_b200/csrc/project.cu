@@ -20,7 +20,6 @@ constexpr int kProjWarps = kProjThreads / 32;
 constexpr int kProjBT = 8;        // requests per pass
 constexpr int kProjMaxRows = 512; // rows per CTA (D / CS)
 constexpr int kProjUnroll = 8;    // row loads in flight per lane
-constexpr int kProjPre = 8;       // rows per lane prefetched before griddepcontrol.wait (256 rows per CTA; 16 measured slower: 254 registers)
 
 #ifndef SALS_PROJ_MINB
 #define SALS_PROJ_MINB 1   // measured: an uncapped register budget (no spills) beats co-residence
@@ -57,16 +56,24 @@ project_kernel(ProjectArgs a) {
   const char* Ub = reinterpret_cast<const char*>(U);
   const size_t row_bytes = (size_t)a.r * sizeof(T);
   const bool rope_role = pool && blockIdx.y == gridDim.y - 1;
-  // U is a weight no upstream kernel writes: issue this lane's first (for
-  // D <= 16 * 256 its only) batch of U rows BEFORE waiting on the upstream
-  // grid, and keep them in registers for every request pass.
+  // U is a weight no upstream kernel writes: the CTA's whole U slice
+  // (rows [row0, row1) x its CPB columns, 128 B per row) is copied into shared
+  // memory by cp.async BEFORE waiting on the upstream grid, so no U load is left
+  // on the critical path after the wait, whatever the rows per CTA.
+  extern __shared__ __align__(16) uint8_t sU[];   // [rows_per][128 B]
   const int base0 = row0 + 4 * warp + slot;
-  uint4 pre[kProjPre];
-#pragma unroll
-  for (int u = 0; u < kProjPre; ++u) {
-    const int c = base0 + u * 4 * kProjWarps;
-    pre[u] = (!rope_role && col_ok && c < row1) ? ld_nc_v4(Ub + (size_t)c * row_bytes + col * sizeof(T))
-                                                : make_uint4(0, 0, 0, 0);
+  if (!rope_role) {
+    const int nvec = (row1 - row0) * 8;
+    const uint32_t su = smem_u32(sU);
+    for (int i = tid; i < nvec; i += kProjThreads) {
+      const int rr = i >> 3, cv = i & 7;
+      const int cc = yb * CPB + cv * EPC;
+      const bool okc = cc < ncols;
+      const char* src = Ub + (size_t)(row0 + rr) * row_bytes + (size_t)(okc ? cc : 0) * sizeof(T);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(su + rr * 128 + cv * 16), "l"(src),
+                   "r"(okc ? 16 : 0) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
   __shared__ float2 sth[128];   // (th_hi, th_lo) per rotation pair: indexed per lane, so not from param space
   if (rope_role)
@@ -222,7 +229,8 @@ project_kernel(ProjectArgs a) {
         for (int e = 0; e < EPC; ++e) xs[bb][cv * EPC + e] = v[e];
       }
     }
-    __syncthreads();
+    if (b0 == 0) asm volatile("cp.async.wait_all;" ::: "memory");   // this thread's U copies
+    __syncthreads();                                                  // everyone's copies and xs visible
 
     float acc[kProjBT][EPC];
 #pragma unroll
@@ -230,7 +238,7 @@ project_kernel(ProjectArgs a) {
 #pragma unroll
       for (int e = 0; e < EPC; ++e) acc[bb][e] = 0.f;
     if (col_ok) {
-      // rows handled by this lane: base0 + 32 i (i < kProjPre from the prefetch, then streamed)
+      // rows handled by this lane: base0 + 32 i, from the shared-memory copy of U
       auto fma_row = [&](const uint4& raw, int c) {
         float uf[EPC];
         Elem<T>::unpack(raw, uf);
@@ -241,24 +249,9 @@ project_kernel(ProjectArgs a) {
           for (int e = 0; e < EPC; ++e) acc[bb][e] = fmaf(uf[e], xv, acc[bb][e]);
         }
       };
-#pragma unroll
-      for (int u = 0; u < kProjPre; ++u) {
-        const int c = base0 + u * 4 * kProjWarps;
-        if (c < row1) fma_row(pre[u], c);
-      }
-      for (int base = base0 + kProjPre * 4 * kProjWarps; base < row1; base += 4 * kProjWarps * kProjUnroll) {
-        uint4 raw[kProjUnroll];
-#pragma unroll
-        for (int u = 0; u < kProjUnroll; ++u) {
-          const int c = base + u * 4 * kProjWarps;
-          raw[u] = (c < row1) ? ld_nc_v4(Ub + (size_t)c * row_bytes + col * sizeof(T)) : make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int u = 0; u < kProjUnroll; ++u) {
-          const int c = base + u * 4 * kProjWarps;
-          if (c < row1) fma_row(raw[u], c);
-        }
-      }
+#pragma unroll 4
+      for (int c = base0; c < row1; c += 4 * kProjWarps)
+        fma_row(*reinterpret_cast<const uint4*>(sU + (c - row0) * 128 + cl * 16), c);
     }
     // reduce the 4 row slots of the warp (lanes cl, cl+8, cl+16, cl+24)
 #pragma unroll
