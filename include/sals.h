@@ -151,6 +151,7 @@ sals_status sals_decode(const sals_config* cfg, const void* U, const void* q,
  * rounded to dtype), written straight into the cache rows.  Uses a cuBLAS
  * handle created on the calling thread's first call (the only state the
  * library keeps besides the comm handle).  Not CUDA-graph captured by the tests.
+ * Value rows are copied as dtype: SALS_ERR_UNSUPPORTED with cfg->v_bits 4 / 2.
  */
 sals_status sals_append_latent_bulk(const sals_config* cfg, const void* U, const void* k, const void* v,
                                     int32_t batch, int32_t n_tokens, int64_t start, void* latent_cache,

@@ -671,6 +671,7 @@ sals_status sals_append_latent_bulk(const sals_config* cfg, const void* U, const
   if (!U || !k || !v || !latent_cache || !v_cache) return fail(SALS_ERR_INVALID_ARGUMENT, "NULL tensor argument");
   if (batch < 1 || n_tokens < 1 || cap < 1 || start < 0 || start + n_tokens > cap)
     return fail(SALS_ERR_INVALID_ARGUMENT, "need batch, n_tokens >= 1 and 0 <= start, start + n_tokens <= cap");
+  if (vq_bits(cfg)) return fail(SALS_ERR_UNSUPPORTED, "bulk append writes dtype value rows (v_bits 0 / 16 only)");
   if (sals_prefill_impl(cfg, U, k, v, batch, n_tokens, start, latent_cache, v_cache, cap, stream) != 0)
     return fail(SALS_ERR_CUDA, "%s", sals_prefill_last_error());
   return SALS_OK;
