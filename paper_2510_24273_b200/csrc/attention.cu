@@ -257,6 +257,7 @@ __global__ void merge_kernel(MergeArgs a) {
   const int bh = blockIdx.x;
   const int b = bh / a.n_q, h = bh % a.n_q;
   pdl_wait();
+  pdl_launch_dependents();   // the next kernels' pre-wait prologues only read weights / their own inputs
   const float* base = a.partials + (size_t)bh * a.bh_stride;
   constexpr int kMaxS = 512;
   __shared__ float sw[kMaxS], sl[kMaxS];

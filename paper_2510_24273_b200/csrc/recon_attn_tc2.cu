@@ -360,6 +360,9 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
         mma_commit(&tfull[buf]);
         TSTAMP(8 + it);
       }
+      // all MMAs issued: the next kernel may launch and run its pre-wait prologue
+      // (the projection stages U, a weight) while this CTA's last epilogue runs
+      pdl_launch_dependents();
     }
   } else if (warp == 2) {
     // ======== V rows producer: 32 TMA tile::gather4 of 4 x 512-B rows per tile; also
