@@ -222,14 +222,18 @@ __device__ unsigned long long g_trace[128];
 #define TSTAMP(slot) do {} while (0)
 #endif
 
-// VB: 16 = dtype (bf16) value rows; 4 / 2 = quantised value rows (DESIGN R15):
-// per KV head 128*VB/8 code bytes then 4 (bf16 scale, bf16 zero) pairs.
-template <int G, int STYLE, int VB>
+// VBH: 16 = dtype (bf16) value rows; 4 / 2 = quantised value rows (DESIGN R15):
+// per KV head 128*VB/8 code bytes then 4 (bf16 scale, bf16 zero) pairs;
+// 40 / 20 = the same with the 8-bit recent window (a compile-time variant so the
+// kernels without the window carry none of its code).
+template <int G, int STYLE, int VBH>
 __global__ void __launch_bounds__(kThreads, 1)
 recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_constant__ CUtensorMap tmap_lat,
                       const __grid_constant__ CUtensorMap tmap_v, const __grid_constant__ CUtensorMap tmap_vh,
                       const __grid_constant__ KArgs ka) {
   constexpr int NQH = 2 * G;             // query heads of this CTA (2 KV heads)
+  constexpr int VB = VBH >= 20 ? VBH / 10 : VBH;
+  constexpr bool HPW = VBH >= 20;        // recent-window variant
   constexpr int kVHead = VB == 16 ? kDH * 2 : kDH * VB / 8 + (kDH / 32) * 4;   // value bytes per head-token
   constexpr int kVRow = 2 * kVHead;                                           // bytes of a V tile row (2 heads)
   constexpr int kVRowH = 2 * 144;   // (quantised) 8-bit recent-window row of the 2 heads (DESIGN R15)
@@ -369,7 +373,7 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
     // warms L2 with the next tile's V and latent rows ========
     const char* vb = reinterpret_cast<const char*>(a.v_cache);
     int* idx = sIdxV;
-    const int hp_lim = (VB != 16 && a.hp_window > 0) ? max(0, a.seq_len[b] - a.hp_window) : -1;
+    const int hp_lim = (HPW && a.hp_window > 0) ? max(0, a.seq_len[b] - a.hp_window) : -1;
     for (int it = 0; it < ntile; ++it) {
       const int tile = t_begin + it;
       const int nv = min(kRows, cnt - tile * kRows);
@@ -383,7 +387,7 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
       // quantised values with a recent window: tokens at positions >= s_b - w (a suffix of
       // the ascending tile) are read from the 8-bit ring (slot pos % w) into sVh
       int thp = nv;
-      if constexpr (VB != 16) {
+      if constexpr (HPW) {
         if (hp_lim >= 0) {   // positions from the indices just staged (no second global read)
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -393,7 +397,7 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
           thp = __reduce_min_sync(0xffffffffu, thp);
         }
       }
-      const bool hp_lane = VB != 16 && thp < nv && 4 * lane + 3 >= thp && 4 * lane < nv;
+      const bool hp_lane = HPW && thp < nv && 4 * lane + 3 >= thp && 4 * lane < nv;
       const int n_hp = __popc(__ballot_sync(0xffffffffu, hp_lane));
       if (lane == 0) {
         *s_thp = thp;
@@ -616,7 +620,7 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
                 const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
                 for (int e = 0; e < 4; ++e) vv[e] = make_float2(__uint_as_float(w[e] << 16), __uint_as_float(w[e] & 0xffff0000u));
-              } else if (t0 + j >= thp) {   // 8-bit recent-window row
+              } else if (HPW && t0 + j >= thp) {   // 8-bit recent-window row
                 // group of 4 tokens: [4 x 144 B of head 0 | pad][4 x 144 B of head 1 | pad]
                 const int tt = t0 + j;
                 const uint8_t* rh = sVh + (tt >> 2) * kHGrp + kh * (kHGrp / 2) + (tt & 3) * 144;
@@ -713,10 +717,10 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
   pdl_launch_dependents();
 }
 
-template <int G, int STYLE, int VB>
+template <int G, int STYLE, int VBH>
 cudaError_t launch_t(const CUtensorMap& map, const CUtensorMap& map_lat, const CUtensorMap& map_v,
                      const CUtensorMap& map_vh, const TcArgs& a, int batch, cudaStream_t st) {
-  auto kern = recon_attn_tc2_kernel<G, STYLE, VB>;
+  auto kern = recon_attn_tc2_kernel<G, STYLE, VBH>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(G));
@@ -767,6 +771,8 @@ cudaError_t launch_recon_attn_tc2(const CUtensorMap& map, const CUtensorMap& ml,
     case 4: return style ? tc2::launch_t<4, 1, VB>(map, ml, mv, mvh, a, batch, st) : tc2::launch_t<4, 0, VB>(map, ml, mv, mvh, a, batch, st); \
   }                                                                                                             \
   return cudaErrorInvalidValue;
+  if (a.v_bits == 4 && a.hp_window > 0) { SALS_TC2_VB(40) }
+  if (a.v_bits == 2 && a.hp_window > 0) { SALS_TC2_VB(20) }
   if (a.v_bits == 4) { SALS_TC2_VB(4) }
   if (a.v_bits == 2) { SALS_TC2_VB(2) }
   SALS_TC2_VB(16)
