@@ -58,6 +58,8 @@ def parse():
                          "{0, 1, 31} dense (P:515, P:561-564)")
     ap.add_argument("--v-bits", type=int, default=0, choices=[0, 4, 2],
                     help="quantised value cache (SURVEY §8(f) f1): 4 or 2 bits, groups of 32 channels")
+    ap.add_argument("--comm", choices=["lib", "torch"], default="lib",
+                    help="c4-sharded exchange: the library's sals_decode_sharded or torch.distributed")
     ap.add_argument("--separate-append", action="store_true",
                     help="sals_append_latent + sals_decode per layer instead of the fused sals_append_decode")
     return ap.parse_args()

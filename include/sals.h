@@ -37,7 +37,8 @@ typedef enum {
   SALS_ERR_INVALID_ARGUMENT = 1,   /* shape / pointer / range violation */
   SALS_ERR_UNSUPPORTED = 2,        /* shape outside the kernels' limits (see each call) */
   SALS_ERR_WORKSPACE_TOO_SMALL = 3,
-  SALS_ERR_CUDA = 4
+  SALS_ERR_CUDA = 4,
+  SALS_ERR_NCCL = 5                /* NCCL missing or a collective failed (sals_decode_sharded) */
 } sals_status;
 
 typedef enum { SALS_F32 = 0, SALS_BF16 = 1 } sals_dtype;
@@ -258,6 +259,36 @@ sals_status sals_merge_partials(const sals_config* cfg, const float* partial_all
                                 int32_t batch, void* out, void* stream);
 size_t sals_shard_workspace_bytes(const sals_config* cfg, int32_t batch, int32_t max_local_len,
                                   int32_t world);
+
+/*
+ * The whole sequence-sharded layer-step in one call: the
+ * three phases above around two in-place NCCL all-gathers on `stream`, then
+ * the merge; `out` [B, n_q*d] is identical on every rank.  One process (or
+ * thread) per GPU, every rank calls with the same cfg / batch / max_local_len.
+ *  - sals_comm_unique_id: writes an ncclUniqueId (128 bytes) to HOST memory;
+ *    rank 0 creates it and the caller broadcasts it (e.g. torch.distributed).
+ *  - sals_comm_init: blocking collective over `world` ranks; *comm receives an
+ *    opaque handle owned by the caller until sals_comm_destroy.  Returns
+ *    SALS_ERR_NCCL when libnccl.so.2 cannot be loaded (resolved at run time:
+ *    the copy already in the process if any) or initialisation fails.
+ *  - sals_decode_sharded: arguments as sals_shard_candidates / _attend (rank p
+ *    holds global positions [shard_start, shard_start + local_len_b) of every
+ *    request); workspace of sals_decode_sharded_workspace_bytes(cfg, B,
+ *    max_local_len, world) bytes holds the phases' workspace plus the gathered
+ *    candidates [P, B, k] x (fp32, int32) and partials [P, B, n_q, d+2] fp32.
+ *    With world = 1 the result equals sals_decode's.  The quantised values'
+ *    recent window is not sharded (SALS_ERR_UNSUPPORTED).
+ */
+sals_status sals_comm_unique_id(void* id_out);
+sals_status sals_comm_init(const void* nccl_unique_id, int32_t world, int32_t rank, void** comm);
+sals_status sals_comm_destroy(void* comm);
+size_t sals_decode_sharded_workspace_bytes(const sals_config* cfg, int32_t batch, int32_t max_local_len,
+                                           int32_t world);
+sals_status sals_decode_sharded(const sals_config* cfg, void* comm, const void* U, const void* q,
+                                const void* latent_shard, const void* v_shard, int64_t cap_local,
+                                int32_t batch, int64_t shard_start, const int32_t* d_local_len,
+                                int32_t max_local_len, const int32_t* d_seq_len, void* out,
+                                void* workspace, size_t ws_bytes, void* stream);
 
 const char* sals_status_string(sals_status s);
 const char* sals_last_error(void);

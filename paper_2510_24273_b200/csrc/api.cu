@@ -1,7 +1,11 @@
 // Host side of the C ABI (include/sals.h): argument validation, workspace
 // carving, path / grid planning and stream-ordered launches (programmatic
 // dependent launch, thread-block clusters).  Never allocates, never syncs.
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <atomic>
+#include <cstring>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -557,6 +561,7 @@ const char* sals_status_string(sals_status s) {
     case SALS_ERR_UNSUPPORTED: return "SALS_ERR_UNSUPPORTED";
     case SALS_ERR_WORKSPACE_TOO_SMALL: return "SALS_ERR_WORKSPACE_TOO_SMALL";
     case SALS_ERR_CUDA: return "SALS_ERR_CUDA";
+    case SALS_ERR_NCCL: return "SALS_ERR_NCCL";
   }
   return "SALS_ERR_UNKNOWN";
 }
@@ -918,6 +923,144 @@ sals_status sals_merge_partials(const sals_config* cfg, const float* partial_all
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (cfg->dtype == SALS_BF16) return launch_merge<__nv_bfloat16>(cfg, m, batch, st);
   return launch_merge<float>(cfg, m, batch, st);
+}
+
+}  // extern "C"
+
+// ------------------------------------------- sharded decode with its own NCCL
+// the whole sharded layer-step in one call -- the three device
+// phases above around two in-place NCCL all-gathers on the caller's stream
+// (NVLink / NVSwitch between the GPUs of a node).  NCCL is resolved at run time
+// (dlopen of libnccl.so.2: the copy torch already loaded if there is one), so
+// the library has no link-time NCCL dependency.
+namespace {
+struct NcclFns {
+  decltype(&ncclGetUniqueId) get_id = nullptr;
+  decltype(&ncclCommInitRank) init = nullptr;
+  decltype(&ncclCommDestroy) destroy = nullptr;
+  decltype(&ncclAllGather) all_gather = nullptr;
+  decltype(&ncclGroupStart) group_start = nullptr;
+  decltype(&ncclGroupEnd) group_end = nullptr;
+  decltype(&ncclGetErrorString) err = nullptr;
+  bool ok = false;
+};
+const NcclFns& nccl() {
+  static const NcclFns f = [] {
+    NcclFns n{};
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return n;
+    n.get_id = reinterpret_cast<decltype(n.get_id)>(dlsym(h, "ncclGetUniqueId"));
+    n.init = reinterpret_cast<decltype(n.init)>(dlsym(h, "ncclCommInitRank"));
+    n.destroy = reinterpret_cast<decltype(n.destroy)>(dlsym(h, "ncclCommDestroy"));
+    n.all_gather = reinterpret_cast<decltype(n.all_gather)>(dlsym(h, "ncclAllGather"));
+    n.group_start = reinterpret_cast<decltype(n.group_start)>(dlsym(h, "ncclGroupStart"));
+    n.group_end = reinterpret_cast<decltype(n.group_end)>(dlsym(h, "ncclGroupEnd"));
+    n.err = reinterpret_cast<decltype(n.err)>(dlsym(h, "ncclGetErrorString"));
+    n.ok = n.get_id && n.init && n.destroy && n.all_gather && n.group_start && n.group_end && n.err;
+    return n;
+  }();
+  return f;
+}
+struct SalsComm {
+  ncclComm_t comm;
+  int32_t world, rank;
+};
+#define SALS_NCCL_TRY(expr)                                                              \
+  do {                                                                                   \
+    ncclResult_t r_ = (expr);                                                            \
+    if (r_ != ncclSuccess) return fail(SALS_ERR_NCCL, "%s: %s", #expr, nccl().err(r_)); \
+  } while (0)
+struct ShardLayout {
+  size_t base, cand_s, cand_i, part, part_all, total;
+};
+ShardLayout shard_layout(const sals_config* cfg, int32_t batch, int32_t max_local_len, int32_t world) {
+  ShardLayout L{};
+  L.base = align_up(sals_shard_workspace_bytes(cfg, batch, max_local_len, world), 256);
+  const size_t cand = align_up((size_t)world * batch * cfg->top_k * 4, 256);
+  const size_t part = (size_t)batch * cfg->num_q_heads * (cfg->head_dim + 2) * 4;
+  L.cand_s = L.base;
+  L.cand_i = L.cand_s + cand;
+  L.part_all = L.cand_i + cand;
+  L.total = L.part_all + align_up(part * world, 256);
+  return L;
+}
+}  // namespace
+
+extern "C" {
+
+sals_status sals_comm_unique_id(void* id_out) {
+  if (!id_out) return fail(SALS_ERR_INVALID_ARGUMENT, "NULL id buffer");
+  if (!nccl().ok) return fail(SALS_ERR_NCCL, "libnccl.so.2 not found");
+  SALS_NCCL_TRY(nccl().get_id(reinterpret_cast<ncclUniqueId*>(id_out)));
+  return SALS_OK;
+}
+
+sals_status sals_comm_init(const void* nccl_unique_id, int32_t world, int32_t rank, void** comm) {
+  if (!nccl_unique_id || !comm || world < 1 || rank < 0 || rank >= world)
+    return fail(SALS_ERR_INVALID_ARGUMENT, "bad communicator arguments");
+  if (!nccl().ok) return fail(SALS_ERR_NCCL, "libnccl.so.2 not found");
+  ncclUniqueId id;
+  memcpy(&id, nccl_unique_id, sizeof(id));
+  ncclComm_t c = nullptr;
+  SALS_NCCL_TRY(nccl().init(&c, world, id, rank));
+  *comm = new SalsComm{c, world, rank};
+  return SALS_OK;
+}
+
+sals_status sals_comm_destroy(void* comm) {
+  if (!comm) return SALS_OK;
+  SalsComm* c = reinterpret_cast<SalsComm*>(comm);
+  ncclResult_t r = nccl().destroy(c->comm);
+  delete c;
+  if (r != ncclSuccess) return fail(SALS_ERR_NCCL, "ncclCommDestroy: %s", nccl().err(r));
+  return SALS_OK;
+}
+
+size_t sals_decode_sharded_workspace_bytes(const sals_config* cfg, int32_t batch, int32_t max_local_len,
+                                           int32_t world) {
+  if (sals_shard_workspace_bytes(cfg, batch, max_local_len, world) == 0) return 0;
+  return shard_layout(cfg, batch, max_local_len, world).total;
+}
+
+sals_status sals_decode_sharded(const sals_config* cfg, void* comm, const void* U, const void* q,
+                                const void* latent_shard, const void* v_shard, int64_t cap_local, int32_t batch,
+                                int64_t shard_start, const int32_t* d_local_len, int32_t max_local_len,
+                                const int32_t* d_seq_len, void* out, void* workspace, size_t ws_bytes,
+                                void* stream) {
+  sals_status s = validate(cfg);
+  if (s != SALS_OK) return s;
+  if (!comm) return fail(SALS_ERR_INVALID_ARGUMENT, "NULL communicator");
+  if (!out || !workspace) return fail(SALS_ERR_INVALID_ARGUMENT, "NULL tensor argument");
+  if (batch < 1 || max_local_len < 1) return fail(SALS_ERR_INVALID_ARGUMENT, "bad shard geometry");
+  const SalsComm* c = reinterpret_cast<const SalsComm*>(comm);
+  const int P = c->world, me = c->rank;
+  if (ws_bytes < sals_decode_sharded_workspace_bytes(cfg, batch, max_local_len, P))
+    return fail(SALS_ERR_WORKSPACE_TOO_SMALL, "sharded workspace too small");
+  const ShardLayout L = shard_layout(cfg, batch, max_local_len, P);
+  char* ws = reinterpret_cast<char*>(workspace);
+  const size_t nc = (size_t)batch * cfg->top_k;
+  const size_t np = (size_t)batch * cfg->num_q_heads * (cfg->head_dim + 2);
+  float* cand_s = reinterpret_cast<float*>(ws + L.cand_s);
+  int32_t* cand_i = reinterpret_cast<int32_t*>(ws + L.cand_i);
+  float* part_all = reinterpret_cast<float*>(ws + L.part_all);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  // 1. local candidates straight into this rank's slot of the gather buffers
+  s = sals_shard_candidates(cfg, U, q, latent_shard, cap_local, batch, shard_start, d_local_len, max_local_len,
+                            d_seq_len, cand_s + me * nc, cand_i + me * nc, workspace, L.base, stream);
+  if (s != SALS_OK) return s;
+  // 2. in-place all-gather of (score, index): one NCCL group, rank order
+  SALS_NCCL_TRY(nccl().group_start());
+  SALS_NCCL_TRY(nccl().all_gather(cand_s + me * nc, cand_s, nc, ncclFloat32, c->comm, st));
+  SALS_NCCL_TRY(nccl().all_gather(cand_i + me * nc, cand_i, nc, ncclInt32, c->comm, st));
+  SALS_NCCL_TRY(nccl().group_end());
+  // 3. global selection + attention over the owned tokens -> this rank's partial slot
+  s = sals_shard_attend(cfg, U, q, latent_shard, v_shard, cap_local, batch, shard_start, d_local_len, max_local_len,
+                        d_seq_len, cand_s, cand_i, P, part_all + me * np, workspace, L.base, stream);
+  if (s != SALS_OK) return s;
+  // 4. in-place all-gather of the partials, 5. merge on every rank
+  SALS_NCCL_TRY(nccl().all_gather(part_all + me * np, part_all, np, ncclFloat32, c->comm, st));
+  return sals_merge_partials(cfg, part_all, P, batch, out, stream);
 }
 
 }  // extern "C"

@@ -18,14 +18,15 @@ SALS_F32, SALS_BF16 = 0, 1
 SALS_ROPE_HALF, SALS_ROPE_INTERLEAVED = 0, 1
 SALS_PATH_AUTO, SALS_PATH_SIMT, SALS_PATH_TCGEN05 = 0, 1, 2
 STATUS = {0: "SALS_OK", 1: "SALS_ERR_INVALID_ARGUMENT", 2: "SALS_ERR_UNSUPPORTED",
-          3: "SALS_ERR_WORKSPACE_TOO_SMALL", 4: "SALS_ERR_CUDA"}
+          3: "SALS_ERR_WORKSPACE_TOO_SMALL", 4: "SALS_ERR_CUDA", 5: "SALS_ERR_NCCL"}
 
 EXPORTED = ["sals_workspace_bytes", "sals_append_latent", "sals_decode", "sals_decode_profile", "sals_dense_append",
             "sals_dense_workspace_bytes", "sals_dense_decode", "sals_shard_candidates", "sals_shard_attend",
             "sals_merge_partials", "sals_shard_workspace_bytes", "sals_status_string", "sals_last_error",
             "sals_launch_count", "sals_profile_stage_mask", "sals_append_decode",
             "sals_append_latent_bulk", "sals_calibrate_workspace_bytes", "sals_calibrate",
-            "sals_v_row_bytes", "sals_v_cache_bytes"]
+            "sals_v_row_bytes", "sals_v_cache_bytes", "sals_comm_unique_id", "sals_comm_init",
+            "sals_comm_destroy", "sals_decode_sharded_workspace_bytes", "sals_decode_sharded"]
 
 
 class SalsError(RuntimeError):
@@ -79,6 +80,11 @@ def _load():
         "sals_shard_attend": (I32, [C, P, P, P, P, I64, I32, I64, P, I32, P, P, P, I32, P, P, SZ, P]),
         "sals_merge_partials": (I32, [C, P, I32, I32, P, P]),
         "sals_shard_workspace_bytes": (SZ, [C, I32, I32, I32]),
+        "sals_comm_unique_id": (I32, [P]),
+        "sals_comm_init": (I32, [P, I32, I32, ctypes.POINTER(P)]),
+        "sals_comm_destroy": (I32, [P]),
+        "sals_decode_sharded_workspace_bytes": (SZ, [C, I32, I32, I32]),
+        "sals_decode_sharded": (I32, [C, P, P, P, P, P, I64, I32, I64, P, I32, P, P, P, SZ, P]),
         "sals_status_string": (ctypes.c_char_p, [I32]),
         "sals_last_error": (ctypes.c_char_p, []),
         "sals_launch_count": (ctypes.c_uint64, [I32]),
@@ -214,6 +220,37 @@ def sals_shard_attend(cfg, U, q, latent_shard, v_shard, shard_start, local_len, 
 
 def sals_merge_partials(cfg, partial_all, world, batch, out, stream=None):
     _check(_lib.sals_merge_partials(ctypes.byref(cfg), _p(partial_all), int(world), int(batch), _p(out),
+                                    _stream(stream)))
+
+
+def sals_comm_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it; the caller broadcasts it)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.sals_comm_unique_id(buf))
+    return buf.raw
+
+
+def sals_comm_init(unique_id: bytes, world: int, rank: int) -> ctypes.c_void_p:
+    """Blocking over the `world` ranks; returns the opaque communicator handle."""
+    buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+    comm = ctypes.c_void_p()
+    _check(_lib.sals_comm_init(buf, int(world), int(rank), ctypes.byref(comm)))
+    return comm
+
+
+def sals_comm_destroy(comm) -> None:
+    _check(_lib.sals_comm_destroy(comm))
+
+
+def sals_decode_sharded_workspace_bytes(cfg: sals_config, batch: int, max_local_len: int, world: int) -> int:
+    return int(_lib.sals_decode_sharded_workspace_bytes(ctypes.byref(cfg), batch, max_local_len, world))
+
+
+def sals_decode_sharded(cfg, comm, U, q, latent_shard, v_shard, shard_start, local_len, max_local_len, seq_len, out,
+                        workspace, stream=None):
+    _check(_lib.sals_decode_sharded(ctypes.byref(cfg), comm, _p(U), _p(q), _p(latent_shard), _p(v_shard),
+                                    latent_shard.shape[1], q.shape[0], int(shard_start), _p(local_len),
+                                    int(max_local_len), _p(seq_len), _p(out), _p(workspace), workspace.numel(),
                                     _stream(stream)))
 
 

@@ -116,13 +116,25 @@ def bench(args, rank, world):
     ws = sals.alloc_workspace(sals.sals_shard_workspace_bytes(cfg, B, n_loc, world), "cuda")
     owner = rank == world - 1                       # holds position s-1, appends the new token
     pos_local = (loc - 1).to(torch.int32)
-    decs = [ShardedDecoder(gpu_phases(cfg, ly["U"], ly["q"], seq, n_loc, ws, world)) for ly in layers]
+    comm = None
+    if args.comm == "lib":   # the library's one-call path with its own NCCL communicator
+        uid = [sals.sals_comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = sals.sals_comm_init(uid[0], world, rank)
+        ws = sals.alloc_workspace(sals.sals_decode_sharded_workspace_bytes(cfg, B, n_loc, world), "cuda")
+        outs = [torch.empty(B, ly["q"].shape[1], dtype=ly["q"].dtype, device="cuda") for ly in layers]
+    else:
+        decs = [ShardedDecoder(gpu_phases(cfg, ly["U"], ly["q"], seq, n_loc, ws, world)) for ly in layers]
 
     def step():
-        for ly, dec in zip(layers, decs):
+        for i, ly in enumerate(layers):
             if owner:
                 sals.sals_append_latent(cfg, ly["U"], ly["k_new"], ly["v_new"], pos_local, ly["latent"], ly["v"])
-            dec.decode(ly["latent"], ly["v"], start, loc)
+            if comm is not None:
+                sals.sals_decode_sharded(cfg, comm, ly["U"], ly["q"], ly["latent"], ly["v"], start, loc, n_loc, seq,
+                                         outs[i], ws)
+            else:
+                decs[i].decode(ly["latent"], ly["v"], start, loc)
 
     stream = torch.cuda.Stream()
     graph = None
@@ -158,6 +170,11 @@ def bench(args, rank, world):
                 "data": "synthetic",
                 "config": {"workload": f"c4-sharded: B={B} n={s} sequence-sharded over {world} GPUs x{L} layers",
                            "batch": B, "seq_len": s, "layers": L, "parallelism": f"sequence-shard x{world}",
-                           "graph": graph is not None},
+                           "graph": graph is not None,
+                           "exchange": "sals_decode_sharded (library NCCL)" if comm is not None
+                           else "torch.distributed all_gather_into_tensor"},
                 "us_per_layer_step": ms * 1e3 / L}
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        torch.cuda.synchronize()
+        sals.sals_comm_destroy(comm)

@@ -76,6 +76,17 @@ def test_host_validation_without_gpu(lib_path):
     st = sals._lib.sals_append_latent(ctypes.byref(c), None, None, None, 1, None, None, None, 1, None)
     assert st == 1
     assert sals.sals_status_string(3) == "SALS_ERR_WORKSPACE_TOO_SMALL"
+    assert sals.sals_status_string(5) == "SALS_ERR_NCCL"
+    # sharded one-call path: NULL communicator / bad rank rejected before any NCCL or CUDA work
+    st = sals._lib.sals_decode_sharded(ctypes.byref(c), None, None, None, None, None, 1, 1, 0, None, 1, None, None,
+                                       None, 0, None)
+    assert st == 1 and "communicator" in sals.sals_last_error()
+    h = ctypes.c_void_p()
+    assert sals._lib.sals_comm_init(ctypes.create_string_buffer(128), 2, 2, ctypes.byref(h)) == 1
+    assert sals._lib.sals_comm_destroy(None) == 0
+    w1 = sals.sals_decode_sharded_workspace_bytes(c, 1, 16384, 1)
+    w8 = sals.sals_decode_sharded_workspace_bytes(c, 1, 16384, 8)
+    assert w8 > w1 > sals.sals_shard_workspace_bytes(c, 1, 16384, 1) > 0
 
 
 def test_workspace_monotone(lib_path):

@@ -263,6 +263,44 @@ def test_sharded_virtual_ranks_equal_unsharded(P, sink, recent):
     assert np.max(np.abs(H.widen(out) - gpu["out"])) <= 2 ** -6
 
 
+@pytest.mark.parametrize("sink,recent", [(0, 0), (16, 64)])
+def test_decode_sharded_nccl_one_rank(sink, recent):
+    """sals_decode_sharded (phases + in-place NCCL all-gathers inside the library)
+    on a one-rank communicator: the selection of the unsharded decode, the output
+    against the oracle forced to it, and equal to the unsharded output up to the
+    fp32 merge order; also graph-capturable."""
+    from paper_2510_24273_b200 import sals
+    sh = _shape("c4", rank=256, score_rank=128, top_k=1024)
+    B, s = 2, 20000
+    cfg, host, gpu = H.run_sals(sh, B, [s, s - 3333], sink=sink, recent=recent, seed=37)
+    oc = H.oracle_cfg(sh, sink, recent)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda().bfloat16()
+    U, q, lat, vv = dev(host["U"]), dev(host["q"]), dev(host["latent"]), dev(host["v"])
+    seq = torch.from_numpy(host["seq_len"]).cuda()
+    comm = sals.sals_comm_init(sals.sals_comm_unique_id(), 1, 0)
+    try:
+        ws = sals.alloc_workspace(sals.sals_decode_sharded_workspace_bytes(cfg, B, s, 1), "cuda")
+        out = torch.empty(B, sh["num_q_heads"] * sh["head_dim"], dtype=torch.bfloat16, device="cuda")
+        sals.sals_decode_sharded(cfg, comm, U, q, lat, vv, 0, seq, s, seq, out, ws)
+        torch.cuda.synchronize()
+        forced = [gpu["sel"][b][gpu["sel"][b] >= 0].astype(np.int64) for b in range(B)]
+        orc = O.decode(oc, host["U"], host["q"], host["latent"], host["v"], host["seq_len"], forced_selection=forced)
+        H.check_output(H.widen(out), orc["y"], "bf16")
+        assert np.max(np.abs(H.widen(out) - gpu["out"])) <= 2 ** -6
+        first = out.clone()
+        st = torch.cuda.Stream()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(st):
+            with torch.cuda.graph(g, stream=st):
+                sals.sals_decode_sharded(cfg, comm, U, q, lat, vv, 0, seq, s, seq, out, ws, stream=st)
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, first)
+    finally:
+        sals.sals_comm_destroy(comm)
+
+
 # ------------------------------------------------------------------ fused append + decode
 @pytest.mark.parametrize("nkv,G,d,B,seqs", [(8, 4, 128, 3, [3000, 1777, 2048]),   # D = 1024: same clusters
                                           (32, 1, 128, 2, [4096, 2500])])         # D = 4096
