@@ -19,6 +19,7 @@
 // After its last tile the CTA writes y directly (single chunk) or one
 // (m, l, o) partial per (query head, chunk) for merge_kernel.
 #include <cuda.h>
+#include <type_traits>
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
@@ -604,59 +605,70 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
         const int thp = *s_thp;                                            // tokens >= thp: 8-bit window rows
         const float* pp = sP + kh * G * kPS;
         const int tb = 16 * ew;
+        // the window branch only in warps whose 16 tokens reach it (warp-uniform:
+        // thp is per CTA), so the other warps run the plain quantised loop
+        auto pv = [&](auto win) {
+          constexpr bool W = decltype(win)::value;
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const int t0 = tb + 4 * q4;
-          if (t0 >= nv) break;
-          float4 p4[G];
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const int t0 = tb + 4 * q4;
+            if (t0 >= nv) break;
+            float4 p4[G];
 #pragma unroll
-          for (int g = 0; g < G; ++g) p4[g] = *reinterpret_cast<const float4*>(pp + g * kPS + t0);
+            for (int g = 0; g < G; ++g) p4[g] = *reinterpret_cast<const float4*>(pp + g * kPS + t0);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            if (t0 + j < nv) {
-              float2 vv[4];   // the lane's 8 values (dims 8 (lane & 15) .. + 8 of KV head kh)
-              if constexpr (VB == 16) {
-                const uint4 v = vrow[(t0 + j) * 32];
-                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+            for (int j = 0; j < 4; ++j) {
+              if (t0 + j < nv) {
+                float2 vv[4];   // the lane's 8 values (dims 8 (lane & 15) .. + 8 of KV head kh)
+                if constexpr (VB == 16) {
+                  const uint4 v = vrow[(t0 + j) * 32];
+                  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                for (int e = 0; e < 4; ++e) vv[e] = make_float2(__uint_as_float(w[e] << 16), __uint_as_float(w[e] & 0xffff0000u));
-              } else if (HPW && t0 + j >= thp) {   // 8-bit recent-window row
-                // group of 4 tokens: [4 x 144 B of head 0 | pad][4 x 144 B of head 1 | pad]
-                const int tt = t0 + j;
-                const uint8_t* rh = sVh + (tt >> 2) * kHGrp + kh * (kHGrp / 2) + (tt & 3) * 144;
-                const int l8 = lane & 15;
-                const uint32_t par = *reinterpret_cast<const uint32_t*>(rh + 128 + 4 * (l8 >> 2));
-                const float sf = __uint_as_float(par << 16), zf = __uint_as_float(par & 0xffff0000u);
-                const uint2 cw = *reinterpret_cast<const uint2*>(rh + 8 * l8);
-                const uint32_t w2[2] = {cw.x, cw.y};
+                  for (int e = 0; e < 4; ++e) vv[e] = make_float2(__uint_as_float(w[e] << 16), __uint_as_float(w[e] & 0xffff0000u));
+                } else if (W && t0 + j >= thp) {   // 8-bit recent-window row
+                  // group of 4 tokens: [4 x 144 B of head 0 | pad][4 x 144 B of head 1 | pad]
+                  const int tt = t0 + j;
+                  const uint8_t* rh = sVh + (tt >> 2) * kHGrp + kh * (kHGrp / 2) + (tt & 3) * 144;
+                  const int l8 = lane & 15;
+                  const uint32_t par = *reinterpret_cast<const uint32_t*>(rh + 128 + 4 * (l8 >> 2));
+                  const float sf = __uint_as_float(par << 16), zf = __uint_as_float(par & 0xffff0000u);
+                  const uint2 cw = *reinterpret_cast<const uint2*>(rh + 8 * l8);
+                  const uint32_t w2[2] = {cw.x, cw.y};
 #pragma unroll
-                for (int e = 0; e < 4; ++e)
-                  vv[e] = make_float2(fmaf(sf, (float)((w2[e >> 1] >> (16 * (e & 1))) & 255u), zf),
-                                      fmaf(sf, (float)((w2[e >> 1] >> (16 * (e & 1) + 8)) & 255u), zf));
-              } else {
-                const uint8_t* rq = qrow + (t0 + j) * kVRow;
-                const int l8 = lane & 15;
-                const uint32_t par = *reinterpret_cast<const uint32_t*>(rq + 128 * VB / 8 + 4 * (l8 >> 2));
-                const float sf = __uint_as_float(par << 16), zf = __uint_as_float(par & 0xffff0000u);
-                uint32_t cw;
-                if constexpr (VB == 4) cw = *reinterpret_cast<const uint32_t*>(rq + 4 * l8);
-                else cw = *reinterpret_cast<const uint16_t*>(rq + 2 * l8);
-                constexpr uint32_t m = (1u << VB) - 1;
+                  for (int e = 0; e < 4; ++e)
+                    vv[e] = make_float2(fmaf(sf, (float)((w2[e >> 1] >> (16 * (e & 1))) & 255u), zf),
+                                        fmaf(sf, (float)((w2[e >> 1] >> (16 * (e & 1) + 8)) & 255u), zf));
+                } else {
+                  const uint8_t* rq = qrow + (t0 + j) * kVRow;
+                  const int l8 = lane & 15;
+                  const uint32_t par = *reinterpret_cast<const uint32_t*>(rq + 128 * VB / 8 + 4 * (l8 >> 2));
+                  const float sf = __uint_as_float(par << 16), zf = __uint_as_float(par & 0xffff0000u);
+                  uint32_t cw;
+                  if constexpr (VB == 4) cw = *reinterpret_cast<const uint32_t*>(rq + 4 * l8);
+                  else cw = *reinterpret_cast<const uint16_t*>(rq + 2 * l8);
+                  constexpr uint32_t m = (1u << VB) - 1;
 #pragma unroll
-                for (int e = 0; e < 4; ++e)
-                  vv[e] = make_float2(fmaf(sf, (float)((cw >> (2 * e * VB)) & m), zf),
-                                      fmaf(sf, (float)((cw >> ((2 * e + 1) * VB)) & m), zf));
-              }
+                  for (int e = 0; e < 4; ++e)
+                    vv[e] = make_float2(fmaf(sf, (float)((cw >> (2 * e * VB)) & m), zf),
+                                        fmaf(sf, (float)((cw >> ((2 * e + 1) * VB)) & m), zf));
+                }
 #pragma unroll
-              for (int g = 0; g < G; ++g) {
-                const float pj = j == 0 ? p4[g].x : j == 1 ? p4[g].y : j == 2 ? p4[g].z : p4[g].w;
-                lp[g] += pj;
-                const float2 p2 = make_float2(pj, pj);
+                for (int g = 0; g < G; ++g) {
+                  const float pj = j == 0 ? p4[g].x : j == 1 ? p4[g].y : j == 2 ? p4[g].z : p4[g].w;
+                  lp[g] += pj;
+                  const float2 p2 = make_float2(pj, pj);
 #pragma unroll
-                for (int e = 0; e < 4; ++e) ov[g][e] = __ffma2_rn(p2, vv[e], ov[g][e]);
+                  for (int e = 0; e < 4; ++e) ov[g][e] = __ffma2_rn(p2, vv[e], ov[g][e]);
+                }
               }
             }
           }
+        };
+        if constexpr (HPW) {
+          if (tb + 16 <= thp) pv(std::false_type{});
+          else pv(std::true_type{});
+        } else {
+          pv(std::false_type{});
         }
       }
       bar_epi();                                       // sV / sP / sL / sRed / sAl free

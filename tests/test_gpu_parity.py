@@ -492,7 +492,7 @@ def _unpack8(rows, nkv):
     return O.dequantize_values(codes, to_f(par[..., 0]).reshape(*lead, -1), to_f(par[..., 1]).reshape(*lead, -1), 32)
 
 
-@pytest.mark.parametrize("bits,nkv,G,z", [(4, 8, 4, 64), (2, 4, 1, 100)])
+@pytest.mark.parametrize("bits,nkv,G,z", [(4, 8, 4, 64), (2, 4, 1, 100), (4, 8, 2, 20), (2, 8, 4, 128)])
 def test_quantized_values_recent_window(bits, nkv, G, z):
     """Quantised values with the high-precision recent window: the forced
     recent z tokens are read from the 8-bit ring, the rest from the b-bit rows; the
