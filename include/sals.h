@@ -7,7 +7,10 @@
  * Conventions shared by every entry point
  *  - Tensor arguments are DEVICE pointers (cudaMalloc / torch CUDA storage)
  *    owned by the caller, row-major, 16-byte aligned, contiguous.  The
- *    library allocates nothing and keeps no state between calls.
+ *    decode path allocates nothing and keeps no state between calls (the
+ *    exceptions: the opaque communicator of sals_comm_init, owned by the
+ *    caller, and the thread-local cuBLAS / cuSOLVER handles the prefill and
+ *    calibration calls create on first use).
  *  - `stream` is a cudaStream_t passed as void*.  Every call only enqueues
  *    work on that stream (no host synchronisation), so all calls are CUDA-graph
  *    capturable.  Kernels are launched with programmatic dependent launch.
