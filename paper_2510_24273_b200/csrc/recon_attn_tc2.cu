@@ -337,6 +337,9 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
         for (int kc = 0; kc < nk; ++kc, ++u) {
           const int s = u % kStages;
           if (u >= kStages) mbar_wait(&empty[s], ((u / kStages) - 1) & 1);
+#ifdef SALS_EXP_NO_U   // experiment (trace builds only): U fetched for the first stages only
+          if (u >= kStages) { mbar_arrive(&full[s]); continue; }
+#endif
           mbar_arrive_expect_tx(&full[s], kBBytes);
           tma_load_2d(smem_u32(sB + s * kBBytes), &tmap_u, kc * kBK, n0, &full[s]);
         }
