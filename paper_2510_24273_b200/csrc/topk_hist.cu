@@ -73,9 +73,14 @@ __device__ __forceinline__ void warp_prefix(int (*wc)[4], int q0, int* tot) {
 __device__ __forceinline__ void digit_search256(const uint32_t* hist, int rem, int* s_digit, int* s_need,
                                                 int* s_cnt) {
   const int lane = threadIdx.x & 31;
-  int c8[8], tot = 0;
+  // the lane's 8 bins are 32 contiguous bytes: two 16-byte loads (a per-bin
+  // strided read would put 8 lanes on each bank)
+  const uint4* h4 = reinterpret_cast<const uint4*>(hist) + (248 - 8 * lane) / 4;
+  const uint4 lo = h4[0], hi = h4[1];
+  const int c8[8] = {(int)hi.w, (int)hi.z, (int)hi.y, (int)hi.x, (int)lo.w, (int)lo.z, (int)lo.y, (int)lo.x};
+  int tot = 0;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) { c8[j] = (int)hist[255 - 8 * lane - j]; tot += c8[j]; }
+  for (int j = 0; j < 8; ++j) tot += c8[j];
   int incl = tot;
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
@@ -111,7 +116,7 @@ topk_hist_kernel(TopkArgs a) {
   constexpr int kSurvMax = 128;                    // exact brute-force select below this many survivors
   extern __shared__ __align__(16) uint8_t tk_smem[];
   __shared__ uint32_t inc_hist[2][kMaxCluster][256];   // overflow path: [pass parity][source rank][digit]
-  __shared__ uint32_t hist[2][256];
+  __shared__ __align__(16) uint32_t hist[2][256];
   __shared__ uint32_t surv[kSurvMax];
   __shared__ __align__(8) uint64_t cand_bar;           // peers' candidate segments landed (bulk copies)
   __shared__ int inc_cnt[kMaxCluster][4];              // [source rank]: def0, cand, gt, eq
