@@ -876,6 +876,7 @@ sals_status sals_shard_attend(const sals_config* cfg, const void* U, const void*
     return fail(SALS_ERR_INVALID_ARGUMENT, "NULL tensor argument");
   if (world < 1 || batch < 1 || max_local_len < 1 || max_local_len > cap_local)
     return fail(SALS_ERR_INVALID_ARGUMENT, "bad shard geometry");
+  if (hp_window(cfg)) return fail(SALS_ERR_UNSUPPORTED, "the quantised values' recent window is not sharded");
   Plan p{};
   s = make_plan(cfg, batch, max_local_len, p, false);
   if (s != SALS_OK) return s;
@@ -902,7 +903,6 @@ sals_status sals_shard_attend(const sals_config* cfg, const void* U, const void*
   oa.gsel = gsel; oa.gcount = gcount; oa.g_stride = cfg->top_k; oa.seq_len = d_seq_len; oa.local_len = d_local_len;
   oa.shard_start = shard_start; oa.sink = cfg->sink; oa.recent = cfg->recent; oa.k = cfg->top_k;
   oa.own_sel = own; oa.own_count = own_count;
-  if (hp_window(cfg)) return fail(SALS_ERR_UNSUPPORTED, "the quantised values' recent window is not sharded");
   SALS_CUDA_TRY(launch(owned_list_kernel, dim3(batch), dim3(256), 0, st, 0, oa));
   if (cfg->dtype == SALS_BF16)
     return attend_list<__nv_bfloat16>(cfg, p, U, latent_shard, v_shard, cap_local, batch, shard_start, own,
@@ -1030,9 +1030,13 @@ sals_status sals_decode_sharded(const sals_config* cfg, void* comm, const void* 
                                 void* stream) {
   sals_status s = validate(cfg);
   if (s != SALS_OK) return s;
+  // everything the later phases check, checked before the first one enqueues work
   if (!comm) return fail(SALS_ERR_INVALID_ARGUMENT, "NULL communicator");
-  if (!out || !workspace) return fail(SALS_ERR_INVALID_ARGUMENT, "NULL tensor argument");
-  if (batch < 1 || max_local_len < 1) return fail(SALS_ERR_INVALID_ARGUMENT, "bad shard geometry");
+  if (!U || !q || !latent_shard || !v_shard || !d_local_len || !d_seq_len || !out || !workspace)
+    return fail(SALS_ERR_INVALID_ARGUMENT, "NULL tensor argument");
+  if (batch < 1 || max_local_len < 1 || max_local_len > cap_local || shard_start < 0)
+    return fail(SALS_ERR_INVALID_ARGUMENT, "bad shard geometry");
+  if (hp_window(cfg)) return fail(SALS_ERR_UNSUPPORTED, "the quantised values' recent window is not sharded");
   const SalsComm* c = reinterpret_cast<const SalsComm*>(comm);
   const int P = c->world, me = c->rank;
   if (ws_bytes < sals_decode_sharded_workspace_bytes(cfg, batch, max_local_len, P))

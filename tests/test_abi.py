@@ -81,6 +81,12 @@ def test_host_validation_without_gpu(lib_path):
     st = sals._lib.sals_decode_sharded(ctypes.byref(c), None, None, None, None, None, 1, 1, 0, None, 1, None, None,
                                        None, 0, None)
     assert st == 1 and "communicator" in sals.sals_last_error()
+    # the window of quantised values is not sharded: refused before anything is enqueued
+    cw = _cfg(sals, v_bits=4, recent=64)
+    fake = ctypes.c_void_p(256)
+    st = sals._lib.sals_decode_sharded(ctypes.byref(cw), fake, fake, fake, fake, fake, 4096, 1, 0, fake, 4096, fake,
+                                       fake, fake, 1 << 30, None)
+    assert st == 2 and "window" in sals.sals_last_error()
     h = ctypes.c_void_p()
     assert sals._lib.sals_comm_init(ctypes.create_string_buffer(128), 2, 2, ctypes.byref(h)) == 1
     assert sals._lib.sals_comm_destroy(None) == 0
