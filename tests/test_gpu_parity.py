@@ -497,12 +497,23 @@ def test_quantized_values_recent_window(bits, nkv, G, z):
     """Quantised values with the high-precision recent window: the forced
     recent z tokens are read from the 8-bit ring, the rest from the b-bit rows; the
     append writes both formats.  Checked against the oracle over the stored V^."""
+    _quantized_window_case(bits, nkv, G, z, seqs=[3000, 2311], k=384, rank=256, rstar=128, seed=23)
+
+
+def test_quantized_values_recent_window_c3_size():
+    """The same at c3's shape (Mistral-7B GQA 32/8, r 512, r* 256, k 4096, 32K tokens)
+    with the paper's Mistral recent window z = 128, 4-bit values."""
+    _quantized_window_case(4, 8, 4, 128, seqs=[32768, 30001], k=4096, rank=512, rstar=256, seed=29)
+
+
+def _quantized_window_case(bits, nkv, G, z, seqs, k, rank, rstar, seed):
     from paper_2510_24273_b200 import sals
-    d, B, seqs, k = 128, 2, [3000, 2311], 384
-    sh = dict(num_q_heads=nkv * G, num_kv_heads=nkv, head_dim=d, rank=256, score_rank=128, top_k=k,
+    d, B = 128, len(seqs)
+    sh = dict(num_q_heads=nkv * G, num_kv_heads=nkv, head_dim=d, rank=rank, score_rank=rstar, top_k=k,
               rope_base=1e6, dtype="bf16")
     cfg = sals.make_config(**sh, v_bits=bits, recent=z)
-    p = synth.gen_problem(num_q_heads=nkv * G, num_kv_heads=nkv, head_dim=d, rank=256, batch=B, seq_lens=seqs, seed=23)
+    p = synth.gen_problem(num_q_heads=nkv * G, num_kv_heads=nkv, head_dim=d, rank=rank, batch=B, seq_lens=seqs,
+                          seed=seed)
     cap = max(seqs)
     dev = lambda a: torch.from_numpy(a).cuda().bfloat16()
     U, q, kn, vn, lat = dev(p["U"]), dev(p["q"]), dev(p["k_new"]), dev(p["v_new"]), dev(p["latent"])
