@@ -341,6 +341,30 @@ def test_memory_model_matches_paper_table2_and_p427():
         assert abs(1.0 / c["table2_access"] - c["p427_reduction"]) < 0.01
 
 
+def test_roofline_numerators_match_survey_sizes():
+    """The per-launch work the bench divides by kernel time (traffic.stage_bytes /
+    recon_flops) against the sizes SURVEY §8(a) lists for c2 / c3 / c4: latent
+    reads of the score stage 16 / 64 / 64 MiB (a3), gathered latent rows 4 / 16 /
+    16 MiB and the reconstruction GEMM 4096x4096x512 / 16384x1024x512 = 17.18
+    GFLOP each (a5), gathered V rows 32 MiB each (a7), U 4 / 1 / 1 MiB."""
+    from paper_2510_24273_b200 import traffic
+    MiB = 1 << 20
+    want = {"c2": (16, 4, 32, 4), "c3": (64, 16, 32, 1), "c4": (64, 16, 32, 1)}
+    for name, (score_mib, lat_mib, v_mib, u_mib) in want.items():
+        sh = dict(synth.CONFIGS[name])
+        kw = dict(batch=sh["batch"], seq=sh["seq"], num_q_heads=sh["num_q_heads"], num_kv_heads=sh["num_kv_heads"],
+                  head_dim=sh["head_dim"], rank=sh["rank"], score_rank=sh["score_rank"], top_k=sh["top_k"])
+        b = traffic.stage_bytes(**kw)
+        B, s = sh["batch"], sh["seq"]
+        assert b["score"] == score_mib * MiB + B * s * 4          # + the fp32 scores written
+        assert b["recon_attn"] == (lat_mib + u_mib + v_mib) * MiB
+        assert abs(traffic.recon_flops(**kw) / 1e9 - 17.18) < 0.01
+        # 4-bit values (R15): 128 * 4 / 8 code bytes + 4 (scale, zero) pairs per head-token
+        vq = sh["num_kv_heads"] * (64 + 16)
+        bq = traffic.stage_bytes(**kw, v_row_bytes=vq)
+        assert bq["recon_attn"] == b["recon_attn"] - v_mib * MiB + B * min(sh["top_k"], s) * vq
+
+
 # ------------------------------------------------------------------ calibration (Sec. 4.2, Lemma 1)
 def test_calibrate_eigenpairs_and_ky_fan():
     """U_r from calibrate() satisfies C U = U diag(w_:r) (the eigen-equation, not a
