@@ -91,6 +91,10 @@ size_t sals_v_row_bytes(const sals_config* cfg);
  * pos % w; the decode reads positions >= s_b - w from it.  Not with the sharded
  * calls. */
 size_t sals_v_cache_bytes(const sals_config* cfg, int32_t batch, int64_t cap);
+/* The ring sits at byte offset batch * cap * sals_v_row_bytes(cfg) of the value
+ * cache, so with v_bits 4 / 2 and recent > 0, sals_append_latent, sals_decode and
+ * sals_append_decode must be called with the `batch` the cache was allocated for
+ * (a call on the first B' < B requests would address another ring). */
 
 /* Bytes of device workspace sals_decode needs for `batch` requests of at most
  * `max_seq_len` tokens.  0 on invalid arguments. */
@@ -136,7 +140,7 @@ sals_status sals_append_latent(const sals_config* cfg, const void* U, const void
  *   sel_idx_out  [B, k] int32 or NULL: C_b ascending, -1 padded past min(k, s_b)
  *   scores_out   [B, max_seq_len] fp32 or NULL: p' (debug / parity)
  *   workspace    >= sals_workspace_bytes(cfg, batch, max_seq_len) bytes, 256-B aligned
- * Limits (SALS_ERR_UNSUPPORTED): max_seq_len <= 393216, batch <= 65535,
+ * Limits (SALS_ERR_UNSUPPORTED): max_seq_len <= 380928 (16-CTA top-k cluster), batch <= 65535,
  * n_q/n_kv <= 8.
  */
 sals_status sals_decode(const sals_config* cfg, const void* U, const void* q,
@@ -185,8 +189,12 @@ sals_status sals_calibrate(const sals_config* cfg, const void* K, int64_t n_rows
  * (k~ = U^T k_new) and value row are written at slot d_seq_len[b] - 1, and the
  * append's projection shares one launch with the query projection (U is read
  * once for both).  Arguments as for the two calls; latent_cache and v_cache are
- * written (row d_seq_len[b] - 1 only).  Results are identical to
- * sals_append_latent(..., d_pos = d_seq_len - 1, ...) then sals_decode(...).
+ * written (row d_seq_len[b] - 1 only).  The cache rows it writes are identical to
+ * sals_append_latent(..., d_pos = d_seq_len - 1, ...)'s; the decode that follows is
+ * sals_decode's arithmetic, except that for D > 2048 the shared launch splits the
+ * query projection over a different cluster shape (fp32 summation order of q~ and
+ * hence of the scores may differ in the last bits; the selection then agrees except
+ * inside the tie band).  Parity against the oracle is tested for this call itself.
  */
 sals_status sals_append_decode(const sals_config* cfg, const void* U, const void* k_new, const void* v_new,
                                const void* q, void* latent_cache, void* v_cache, int64_t cap, int32_t batch,
@@ -235,6 +243,9 @@ sals_status sals_dense_decode(const sals_config* cfg, const void* q, const void*
  *     ascending index order, padded with (idx -1, score -inf) to k entries.
  *       cand_score [B, k] fp32, cand_idx [B, k] int32 (outputs)
  *  2. (caller) all-gather -> cand_all_* [P, B, k] in rank order.
+ *     It also leaves the rotated query q^R in `workspace`, which phase 3 reads:
+ *     sals_shard_attend must be given the SAME workspace, unmodified in between
+ *     (sals_decode_sharded does this itself).
  *  3. sals_shard_attend: global TopK over the P*k candidates with the same
  *     policy and tie-break as sals_decode (identical on every rank), then
  *     reconstruct + RoPE + attention over the OWNED selected tokens (plus the

@@ -367,17 +367,25 @@ def quantize_values(v: np.ndarray, bits: int, group: int = 32):
     channels shares zero = min and scale = (max - min) / (2^bits - 1), both stored
     in bfloat16; code = clamp(round((v - zero) / scale), 0, 2^bits - 1) computed
     from the stored (rounded) zero / scale; scale 0 -> code 0.
-    v [..., D] -> (codes [..., D] int, scale [..., D/group], zero [..., D/group])."""
-    v = np.asarray(v, dtype=np.float64)
-    g = v.reshape(*v.shape[:-1], v.shape[-1] // group, group)
+
+    Precision (R15): the codes are integers decided by floating point, so the
+    decision is taken in the kernel's precision, IEEE fp32 with round-to-nearest-
+    even: v is the stored value (bf16 / fp32, exact in fp32); hi - lo, the
+    division by 2^bits - 1, v - zero and the division by scale are single fp32
+    operations; the scale is rounded fp32 -> bf16 (nearest-even); round() is
+    half-to-even.  v [..., D] -> (codes [..., D] int, scale [..., D/group],
+    zero [..., D/group]) with scale / zero as float64 (exact bf16 values)."""
+    v32 = np.asarray(v, dtype=np.float32)
+    g = v32.reshape(*v32.shape[:-1], v32.shape[-1] // group, group)
     lo, hi = g.min(-1), g.max(-1)
     qmax = (1 << bits) - 1
-    zero = bf16_round(lo)
-    scale = bf16_round((hi - lo) / qmax)
-    safe = np.where(scale > 0, scale, 1.0)
-    codes = np.clip(np.rint((g - zero[..., None]) / safe[..., None]), 0, qmax)
+    zero = bf16_round(lo).astype(np.float32)
+    scale = bf16_round((hi - lo) / np.float32(qmax)).astype(np.float32)
+    safe = np.where(scale > 0, scale, np.float32(1.0)).astype(np.float32)
+    q = (g - zero[..., None]) / safe[..., None]                      # fp32 subtract, fp32 divide
+    codes = np.clip(np.rint(q), 0, qmax)
     codes = np.where(scale[..., None] > 0, codes, 0).astype(np.int64)
-    return codes.reshape(v.shape), scale, zero
+    return codes.reshape(v32.shape), scale.astype(np.float64), zero.astype(np.float64)
 
 
 def dequantize_values(codes: np.ndarray, scale: np.ndarray, zero: np.ndarray, group: int = 32) -> np.ndarray:
@@ -385,3 +393,20 @@ def dequantize_values(codes: np.ndarray, scale: np.ndarray, zero: np.ndarray, gr
     c = np.asarray(codes, dtype=np.float64)
     g = c.reshape(*c.shape[:-1], c.shape[-1] // group, group)
     return (np.asarray(zero, np.float64)[..., None] + np.asarray(scale, np.float64)[..., None] * g).reshape(c.shape)
+
+
+def value_hat(v_rows: np.ndarray, bits: int, recent: int, s: int, group: int = 32) -> np.ndarray:
+    """The V^ of Algorithm 1 as the quantised cache holds it for a request of
+    s tokens (reading R15): positions j >= s - z (the recent window, whose
+    tokens "are compressed by only 50%" = 8-bit codes on the same grid
+    rule) are reconstructed from 8-bit codes, all earlier positions from `bits`-bit
+    codes; bits = 16 keeps the stored values (no quantisation).  v_rows [>= s, D] ->
+    [s, D] float64."""
+    v = np.asarray(v_rows, dtype=np.float64)[:s]
+    if bits == 16:
+        return v.copy()
+    out = dequantize_values(*quantize_values(v, bits, group), group)
+    z = min(max(recent, 0), s)
+    if z > 0:
+        out[s - z:] = dequantize_values(*quantize_values(v[s - z:], 8, group), group)
+    return out

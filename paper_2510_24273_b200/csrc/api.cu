@@ -15,6 +15,7 @@
 #include "../../include/sals.h"
 #include "kernels.h"
 #include "recon_attn_tc.h"
+#include "once.h"
 
 using namespace sals;
 
@@ -183,6 +184,8 @@ bool tc_eligible(const sals_config* c, int batch, int kmax) {
 // Top-k cluster plan.  cand == true: the generic kernel over all-gathered
 // candidates (K9); else the histogram-assisted kernel (K4 / K8).
 constexpr size_t kTopkDynSmem = 190 * 1024;
+// 16-CTA cluster x 23808-entry slices: slice * 8 B + 1024 candidates x 4 B = 190 KB (plan_topk)
+constexpr int kMaxSeqLen = 16 * 23808;
 sals_status plan_topk(int n_entries, bool cand, Plan& p) {
   static const int slice_env = [] { const char* e = getenv("SALS_TOPK_SLICE"); return e ? atoi(e) : 0; }();
   const int target = (slice_env >= 256 && slice_env <= 16384) ? slice_env : 2048;   // experiment override
@@ -201,7 +204,13 @@ sals_status plan_topk(int n_entries, bool cand, Plan& p) {
     p.tk_smem = ((size_t)slice * 9 + 15) / 16 * 16 + (size_t)(kTopkThreads / 32) * 256 * 4;
   } else {
     p.tk_nt = slice >= 4096 ? 1024 : 512;
-    p.tk_cap = (int)std::min<size_t>(kCandCap, (kTopkDynSmem - (size_t)slice * 8) / 4);
+    // signed: the staged slice (8 B per entry) plus a candidate area of at least
+    // kMinCand entries must fit the kernel's dynamic shared memory
+    constexpr int64_t kMinCand = 1024;
+    const int64_t avail = (int64_t)kTopkDynSmem - (int64_t)slice * 8;
+    if (avail < kMinCand * 4)
+      return fail(SALS_ERR_UNSUPPORTED, "top-k over %d entries exceeds the cluster's shared memory", n_entries);
+    p.tk_cap = (int)std::min<int64_t>(kCandCap, avail / 4);
     p.tk_smem = (size_t)slice * 8 + (size_t)p.tk_cap * 4;
   }
   return SALS_OK;
@@ -292,16 +301,17 @@ sals_status launch_project(const sals_config* c, const Plan& p, int mode, Projec
   else if (mode == 1) gy = ceil_div(a.ncols, cpb) + 1;
   else { a.n_append_blocks = ceil_div(a.ncols_a, cpb); gy = a.n_append_blocks + ceil_div(a.ncols, cpb) + 1; }
   dim3 grid(p.proj_cs, gy);
-  static bool attr_done = false;
-  if (!attr_done) {
-    SALS_CUDA_TRY(cudaFuncSetAttribute(project_kernel<T, 0>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    SALS_CUDA_TRY(cudaFuncSetAttribute(project_kernel<T, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    SALS_CUDA_TRY(cudaFuncSetAttribute(project_kernel<T, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    SALS_CUDA_TRY(cudaFuncSetAttribute(project_kernel<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    SALS_CUDA_TRY(cudaFuncSetAttribute(project_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    SALS_CUDA_TRY(cudaFuncSetAttribute(project_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    attr_done = true;
-  }
+  static DeviceOnce once;
+  SALS_CUDA_TRY(once.run([] {
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(project_kernel<T, 0>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(project_kernel<T, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(project_kernel<T, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(project_kernel<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(project_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(project_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    return e;
+  }));
   const size_t smem = (size_t)p.proj_rows * 128;   // the CTA's U slice (rows x 128 B)
   if (mode == 0) SALS_CUDA_TRY(launch(project_kernel<T, 0>, grid, dim3(kProjThreads), smem, st, p.proj_cs, a));
   else if (mode == 1) SALS_CUDA_TRY(launch(project_kernel<T, 1>, grid, dim3(kProjThreads), smem, st, p.proj_cs, a));
@@ -312,12 +322,8 @@ sals_status launch_project(const sals_config* c, const Plan& p, int mode, Projec
 template <typename T>
 sals_status launch_score(const sals_config* c, ScoreArgs a, int batch, int max_len, cudaStream_t st) {
   if (sizeof(T) == 2 && g_score_tma) {
-    static int nsm = 0;
-    if (!nsm) {
-      int dev = 0;
-      SALS_CUDA_TRY(cudaGetDevice(&dev));
-      SALS_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    }
+    int nsm = 0;
+    SALS_CUDA_TRY(device_sm_count(&nsm));
     cudaError_t e = launch_score_tma(a, batch, max_len, st, nsm);
     if (e == cudaSuccess) { g_launches.fetch_add(1, std::memory_order_relaxed); return SALS_OK; }
     if (e != cudaErrorNotSupported) return fail(SALS_ERR_CUDA, "score_tma launch: %s", cudaGetErrorString(e));
@@ -352,18 +358,18 @@ sals_status launch_score(const sals_config* c, ScoreArgs a, int batch, int max_l
 }
 
 sals_status launch_topk(TopkArgs a, int batch, const Plan& p, cudaStream_t st) {
-  static bool attr_done = false;
-  if (!attr_done) {
+  static DeviceOnce once;
+  SALS_CUDA_TRY(once.run([] {
     auto* k512 = topk_hist_kernel<512>;
     auto* k1024 = topk_hist_kernel<1024>;
-    SALS_CUDA_TRY(cudaFuncSetAttribute(topk_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTopkDynSmem));
-    SALS_CUDA_TRY(cudaFuncSetAttribute(topk_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    SALS_CUDA_TRY(cudaFuncSetAttribute(k512, cudaFuncAttributeMaxDynamicSharedMemorySize, kTopkDynSmem));
-    SALS_CUDA_TRY(cudaFuncSetAttribute(k512, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    SALS_CUDA_TRY(cudaFuncSetAttribute(k1024, cudaFuncAttributeMaxDynamicSharedMemorySize, kTopkDynSmem));
-    SALS_CUDA_TRY(cudaFuncSetAttribute(k1024, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    attr_done = true;
-  }
+    cudaError_t e = cudaFuncSetAttribute(topk_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTopkDynSmem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(topk_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k512, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTopkDynSmem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k512, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k1024, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTopkDynSmem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k1024, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    return e;
+  }));
   // cluster attribute even for cs == 1 (the kernels use cluster barriers / DSMEM)
   if (a.hist0 == nullptr) {
     SALS_CUDA_TRY(launch(topk_cluster_kernel, dim3(batch * p.tk_cs), dim3(kTopkThreads), p.tk_smem, st, p.tk_cs, a));
@@ -385,11 +391,10 @@ template <typename T>
 sals_status launch_recon_simt(const sals_config* c, ReconArgs a, int batch, int kmax, cudaStream_t st) {
   const int DH = c->head_dim;
   const size_t smem = (size_t)(32 * 33 + DH * 33 + 32 * DH) * 4;
-  static bool attr_done = false;
-  if (!attr_done) {
-    SALS_CUDA_TRY(cudaFuncSetAttribute(recon_rope_simt_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-    attr_done = true;
-  }
+  static DeviceOnce once;
+  SALS_CUDA_TRY(once.run([] {
+    return cudaFuncSetAttribute(recon_rope_simt_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+  }));
   dim3 grid(ceil_div(kmax, 32), c->num_kv_heads, batch);
   SALS_CUDA_TRY(launch(recon_rope_simt_kernel<T>, grid, dim3(256), smem, st, 0, a));
   return SALS_OK;
@@ -628,7 +633,7 @@ sals_status sals_decode(const sals_config* cfg, const void* U, const void* q, co
     return fail(SALS_ERR_INVALID_ARGUMENT, "NULL tensor argument");
   if (batch < 1 || batch > 65535) return fail(SALS_ERR_UNSUPPORTED, "batch %d outside [1, 65535]", batch);
   if (max_seq_len < 1 || max_seq_len > cap) return fail(SALS_ERR_INVALID_ARGUMENT, "need 1 <= max_seq_len <= cap");
-  if (max_seq_len > 393216) return fail(SALS_ERR_UNSUPPORTED, "max_seq_len > 393216");
+  if (max_seq_len > kMaxSeqLen) return fail(SALS_ERR_UNSUPPORTED, "max_seq_len > %d", kMaxSeqLen);
   if (reinterpret_cast<uintptr_t>(workspace) % 256) return fail(SALS_ERR_INVALID_ARGUMENT, "workspace not 256-B aligned");
   Plan p{};
   s = make_plan(cfg, batch, max_seq_len, p, false);
@@ -692,7 +697,7 @@ sals_status sals_append_decode(const sals_config* cfg, const void* U, const void
     return fail(SALS_ERR_INVALID_ARGUMENT, "NULL tensor argument");
   if (batch < 1 || batch > 65535) return fail(SALS_ERR_UNSUPPORTED, "batch %d outside [1, 65535]", batch);
   if (max_seq_len < 1 || max_seq_len > cap) return fail(SALS_ERR_INVALID_ARGUMENT, "need 1 <= max_seq_len <= cap");
-  if (max_seq_len > 393216) return fail(SALS_ERR_UNSUPPORTED, "max_seq_len > 393216");
+  if (max_seq_len > kMaxSeqLen) return fail(SALS_ERR_UNSUPPORTED, "max_seq_len > %d", kMaxSeqLen);
   if (reinterpret_cast<uintptr_t>(workspace) % 256) return fail(SALS_ERR_INVALID_ARGUMENT, "workspace not 256-B aligned");
   Plan p{};
   s = make_plan(cfg, batch, max_seq_len, p, false);

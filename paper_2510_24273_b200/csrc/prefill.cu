@@ -11,13 +11,27 @@
 #include <cuda_runtime.h>
 
 #include <string>
+#include <unordered_map>
 
 #include "../../include/sals.h"
 
 namespace {
 
-thread_local cublasHandle_t g_cublas = nullptr;
+// library handles per (calling thread, device): a handle is bound to the device
+// that was current when it was created
+thread_local std::unordered_map<int, cublasHandle_t> g_cublas;
 thread_local std::string g_prefill_err;
+
+cublasHandle_t cublas_handle() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  auto it = g_cublas.find(dev);
+  if (it != g_cublas.end()) return it->second;
+  cublasHandle_t h = nullptr;
+  if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return nullptr;
+  g_cublas[dev] = h;
+  return h;
+}
 
 }  // namespace
 
@@ -32,11 +46,12 @@ extern "C" int sals_prefill_impl(const sals_config* cfg, const void* U, const vo
   const bool bf16 = cfg->dtype == SALS_BF16;
   const size_t es = bf16 ? 2 : 4;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (!g_cublas && cublasCreate(&g_cublas) != CUBLAS_STATUS_SUCCESS) {
+  cublasHandle_t hb = cublas_handle();
+  if (!hb) {
     g_prefill_err = "cublasCreate failed";
     return 1;
   }
-  if (cublasSetStream(g_cublas, st) != CUBLAS_STATUS_SUCCESS) {
+  if (cublasSetStream(hb, st) != CUBLAS_STATUS_SUCCESS) {
     g_prefill_err = "cublasSetStream failed";
     return 1;
   }
@@ -45,7 +60,7 @@ extern "C" int sals_prefill_impl(const sals_config* cfg, const void* U, const vo
   const cudaDataType_t t = bf16 ? CUDA_R_16BF : CUDA_R_32F;
   char* c0 = reinterpret_cast<char*>(latent_cache) + (size_t)start * r * es;
   cublasStatus_t cs = cublasGemmStridedBatchedEx(
-      g_cublas, CUBLAS_OP_N, CUBLAS_OP_N, r, n_tokens, D, &alpha, U, t, r, 0, k, t, D, (long long)n_tokens * D,
+      hb, CUBLAS_OP_N, CUBLAS_OP_N, r, n_tokens, D, &alpha, U, t, r, 0, k, t, D, (long long)n_tokens * D,
       &beta, c0, t, r, (long long)cap * r, batch, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
   if (cs != CUBLAS_STATUS_SUCCESS) {
     g_prefill_err = "cublasGemmStridedBatchedEx failed (" + std::to_string((int)cs) + ")";
@@ -74,7 +89,9 @@ extern "C" int sals_prefill_impl(const sals_config* cfg, const void* U, const vo
 #include <cuda_bf16.h>
 
 namespace {
-thread_local cusolverDnHandle_t g_cusolver = nullptr;
+thread_local std::unordered_map<int, cusolverDnHandle_t> g_cusolver_by_dev;
+thread_local cusolverDnHandle_t g_cusolver = nullptr;   // the calling thread's handle for the current device
+thread_local cublasHandle_t g_cublas_cur = nullptr;
 
 __global__ void calib_columns_kernel(const float* __restrict__ evec, const float* __restrict__ w, int D, int r,
                                      void* U_out, int bf16, float* eig_out) {
@@ -112,12 +129,21 @@ __global__ void calib_columns_kernel(const float* __restrict__ evec, const float
 }
 
 bool calib_handles(cudaStream_t st) {
-  if (!g_cublas && cublasCreate(&g_cublas) != CUBLAS_STATUS_SUCCESS) { g_prefill_err = "cublasCreate failed"; return false; }
-  if (!g_cusolver && cusolverDnCreate(&g_cusolver) != CUSOLVER_STATUS_SUCCESS) {
-    g_prefill_err = "cusolverDnCreate failed";
-    return false;
+  g_cublas_cur = cublas_handle();
+  if (!g_cublas_cur) { g_prefill_err = "cublasCreate failed"; return false; }
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) { g_prefill_err = "cudaGetDevice failed"; return false; }
+  auto it = g_cusolver_by_dev.find(dev);
+  if (it == g_cusolver_by_dev.end()) {
+    cusolverDnHandle_t h = nullptr;
+    if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) {
+      g_prefill_err = "cusolverDnCreate failed";
+      return false;
+    }
+    it = g_cusolver_by_dev.emplace(dev, h).first;
   }
-  cublasSetStream(g_cublas, st);
+  g_cusolver = it->second;
+  cublasSetStream(g_cublas_cur, st);
   cusolverDnSetStream(g_cusolver, st);
   return true;
 }
@@ -158,7 +184,7 @@ extern "C" int sals_calibrate_impl(const sals_config* cfg, const void* K, int64_
   // C (col-major D x D) = K_cm (D x N, ld D) * K_cm^T
   const float one = 1.f, zero = 0.f;
   const cudaDataType_t t = bf16 ? CUDA_R_16BF : CUDA_R_32F;
-  if (cublasGemmEx(g_cublas, CUBLAS_OP_N, CUBLAS_OP_T, D, D, (int)n_rows, &one, K, t, D, K, t, D, &zero, C,
+  if (cublasGemmEx(g_cublas_cur, CUBLAS_OP_N, CUBLAS_OP_T, D, D, (int)n_rows, &one, K, t, D, K, t, D, &zero, C,
                    CUDA_R_32F, D, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS) {
     g_prefill_err = "Gram matrix GEMM failed";
     return 1;

@@ -142,7 +142,9 @@ project_kernel(ProjectArgs a) {
       // ---- append with channel-wise group quantisation (DESIGN R15): four
       // lanes per 32-channel group (8 channels each, one 16-byte load), min / max by
       // two shuffles; zero = min, scale = (max-min)/qmax, both rounded to bf16 first,
-      // codes from the rounded values (x 1/scale), packed low bits first
+      // codes from the rounded values, packed low bits first.  R15's code rule is
+      // exact IEEE fp32 (the oracle takes the same decisions): one rounded subtract,
+      // one rounded divide (no reciprocal), round half to even, clamp
       const int bits = a.v_bits, qmax = (1 << bits) - 1;
       const int gph = 128 / 32;                       // groups per head (head_dim 128)
       const int hb = 128 * bits / 8 + gph * 4;        // bytes per head in a row
@@ -162,13 +164,12 @@ project_kernel(ProjectArgs a) {
         lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 2)); hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, 2));
         if (!ok) continue;
         const __nv_bfloat16 zb = __float2bfloat16_rn(lo);
-        const __nv_bfloat16 sb = __float2bfloat16_rn(__fdiv_rn(hi - lo, (float)qmax));
+        const __nv_bfloat16 sb = __float2bfloat16_rn(__fdiv_rn(__fsub_rn(hi, lo), (float)qmax));
         const float zf = __bfloat162float(zb), sf = __bfloat162float(sb);
-        const float inv = sf > 0.f ? __frcp_rn(sf) : 0.f;
         uint32_t w = 0;
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const int c = min(qmax, max(0, __float2int_rn((f[e] - zf) * inv)));
+          const int c = sf > 0.f ? min(qmax, max(0, __float2int_rn(__fdiv_rn(__fsub_rn(f[e], zf), sf)))) : 0;
           w |= (uint32_t)c << (e * bits);
         }
         const int pb = a.pos ? a.pos[b] : a.seq_len[b] - 1;
@@ -180,12 +181,12 @@ project_kernel(ProjectArgs a) {
               (uint32_t)__bfloat16_as_ushort(sb) | ((uint32_t)__bfloat16_as_ushort(zb) << 16);
         if (a.hp_window > 0) {
           // high-precision copy of the recent window: 8 bits in ring slot pos % w
-          const __nv_bfloat16 s8 = __float2bfloat16_rn(__fdiv_rn(hi - lo, 255.f));
-          const float s8f = __bfloat162float(s8), inv8 = s8f > 0.f ? __frcp_rn(s8f) : 0.f;
+          const __nv_bfloat16 s8 = __float2bfloat16_rn(__fdiv_rn(__fsub_rn(hi, lo), 255.f));
+          const float s8f = __bfloat162float(s8);
           uint32_t w8[2] = {0, 0};
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            const int c = min(255, max(0, __float2int_rn((f[e] - zf) * inv8)));
+            const int c = s8f > 0.f ? min(255, max(0, __float2int_rn(__fdiv_rn(__fsub_rn(f[e], zf), s8f)))) : 0;
             w8[e >> 2] |= (uint32_t)c << ((e & 3) * 8);
           }
           char* ring = reinterpret_cast<char*>(a.v_cache) + a.hp_ring_off +

@@ -26,6 +26,7 @@
 
 #include "common.cuh"
 #include "recon_attn_tc.h"
+#include "once.h"
 
 namespace sals {
 
@@ -382,12 +383,9 @@ bool get_encoder() {
 template <int DH, int G, int STYLE>
 cudaError_t launch_t(const CUtensorMap& map, const TcArgs& a, int batch, cudaStream_t st) {
   auto kern = recon_attn_tc_kernel<DH, G, STYLE>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static DeviceOnce once;
+  cudaError_t e = once.run([&] { return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes); });
+  if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.ntiles, a.D / kBN, batch);
   cfg.blockDim = dim3(kThreads);

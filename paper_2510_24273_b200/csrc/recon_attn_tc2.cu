@@ -24,6 +24,7 @@
 
 #include "common.cuh"
 #include "recon_attn_tc.h"
+#include "once.h"
 
 namespace sals {
 namespace tc2 {
@@ -736,12 +737,9 @@ template <int G, int STYLE, int VBH>
 cudaError_t launch_t(const CUtensorMap& map, const CUtensorMap& map_lat, const CUtensorMap& map_v,
                      const CUtensorMap& map_vh, const TcArgs& a, int batch, cudaStream_t st) {
   auto kern = recon_attn_tc2_kernel<G, STYLE, VBH>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(G));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static DeviceOnce once;
+  cudaError_t e = once.run([&] { return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(G)); });
+  if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.ntiles, a.D / kBN, batch);
   cfg.blockDim = dim3(kThreads);

@@ -30,6 +30,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "recon_attn_tc.h"
+#include "once.h"
 
 namespace sals {
 namespace stma {
@@ -226,13 +227,10 @@ cudaError_t launch_score_tma(const ScoreArgs& a, int batch, int max_len, cudaStr
     case 128: k = stma::score_tma_kernel<16>; break;
     default: k = stma::score_tma_kernel<32>; break;
   }
-  static bool attr[3] = {false, false, false};
+  static DeviceOnce once[3];
   const int ai = a.rstar == 64 ? 0 : (a.rstar == 128 ? 1 : 2);
-  if (!attr[ai]) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr[ai] = true;
-  }
+  cudaError_t e = once[ai].run([&] { return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
+  if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(std::max(1, std::min(items, nsm)));
   cfg.blockDim = dim3(stma::kThreads);

@@ -27,8 +27,10 @@ def widen(t: torch.Tensor) -> np.ndarray:
 
 
 def run_sals(shape: dict, batch: int, seq_lens, *, seed=synth.SEED_BASE, cap=None, sink=0, recent=0,
-             top_k=None, path=0, rope_style=0, dtype=None):
-    """Generate, append the new token, decode.  Returns (cfg, stored host tensors, gpu results)."""
+             top_k=None, path=0, rope_style=0, dtype=None, fused=False):
+    """Generate, append the new token, decode (``fused``: the one call
+    sals_append_decode that bench.py times, else sals_append_latent + sals_decode).
+    Returns (cfg, stored host tensors, gpu results)."""
     from paper_2510_24273_b200 import sals
     dtype = dtype or shape["dtype"]
     tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
@@ -49,14 +51,18 @@ def run_sals(shape: dict, batch: int, seq_lens, *, seed=synth.SEED_BASE, cap=Non
     v_new = torch.from_numpy(p["v_new"]).to(dev).to(tdt)
     seq = torch.from_numpy(seq_lens).to(dev)
     pos = (seq - 1).to(torch.int32)
-    sals.sals_append_latent(cfg, U, k_new, v_new, pos, latent, v)
     D = shape["num_kv_heads"] * shape["head_dim"]
     max_s = int(seq_lens.max())
     ws = sals.alloc_workspace(sals.sals_workspace_bytes(cfg, batch, max_s), dev)
     out = torch.empty(batch, shape["num_q_heads"] * shape["head_dim"], dtype=tdt, device=dev)
     sel = torch.full((batch, k), -7, dtype=torch.int32, device=dev)
     scores = torch.zeros(batch, max_s, dtype=torch.float32, device=dev)
-    sals.sals_decode(cfg, U, q, latent, v, seq, max_s, out, ws, sel_idx_out=sel, scores_out=scores)
+    if fused:
+        sals.sals_append_decode(cfg, U, k_new, v_new, q, latent, v, seq, max_s, out, ws, sel_idx_out=sel,
+                                scores_out=scores)
+    else:
+        sals.sals_append_latent(cfg, U, k_new, v_new, pos, latent, v)
+        sals.sals_decode(cfg, U, q, latent, v, seq, max_s, out, ws, sel_idx_out=sel, scores_out=scores)
     torch.cuda.synchronize()
     host = dict(U=widen(U), q=widen(q), k_new=widen(k_new), v_new=widen(v_new), latent=widen(latent), v=widen(v),
                 seq_len=seq_lens, D=D)
@@ -129,3 +135,55 @@ def full_check(shape, batch, seq_lens, **kw):
     if nswap == 0:
         check_output(gpu["out"], orc["y"], dtype)
     return dict(swaps=nswap, max_abs=stats[0], mean_rel=stats[1])
+
+
+def sampled_check(shape: dict, batch: int, seq: int, *, sample, seed=synth.SEED_BASE, sink=0, recent=0):
+    """Bench-sized parity: one layer drawn on the device with the bench's generator
+    (synth.gen_layer_torch), the whole batch through sals_append_decode in the launch
+    configuration bench.py times; the append rows of EVERY request against the oracle,
+    and the requests in ``sample`` one by one through the oracle (scores, selection
+    band, output forced to the GPU's C and, when equal, the oracle's own C).  Only the
+    sampled requests' rows are widened to fp64 on the host."""
+    from paper_2510_24273_b200 import sals
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    ly = synth.gen_layer_torch(num_q_heads=shape["num_q_heads"], num_kv_heads=shape["num_kv_heads"],
+                               head_dim=shape["head_dim"], rank=shape["rank"], batch=batch, seq=seq, generator=g)
+    cfg = sals.make_config(**shape, sink=sink, recent=recent)
+    oc = oracle_cfg(shape, sink, recent)
+    k = shape["top_k"]
+    seqd = torch.full((batch,), seq, dtype=torch.int32, device="cuda")
+    ws = sals.alloc_workspace(sals.sals_workspace_bytes(cfg, batch, seq), "cuda")
+    out = torch.empty(batch, shape["num_q_heads"] * shape["head_dim"], dtype=torch.bfloat16, device="cuda")
+    sel = torch.full((batch, k), -7, dtype=torch.int32, device="cuda")
+    scores = torch.zeros(batch, seq, dtype=torch.float32, device="cuda")
+    sals.sals_append_decode(cfg, ly["U"], ly["k_new"], ly["v_new"], ly["q"], ly["latent"], ly["v"], seqd, seq, out,
+                            ws, sel_idx_out=sel, scores_out=scores)
+    torch.cuda.synchronize()
+    U = widen(ly["U"])
+    # append rows of every request (1 bf16 ulp of the fp64 projection; value rows bit-exact)
+    ref = O.project_latent(U, widen(ly["k_new"]))
+    rows = widen(ly["latent"][:, seq - 1])
+    ulp = 2.0 ** (np.floor(np.log2(np.maximum(np.abs(ref), 1e-30))) - 7)
+    assert np.all(np.abs(rows - ref) <= ulp + 1e-6), np.max(np.abs(rows - ref) / ulp)
+    assert torch.equal(ly["v"][:, seq - 1], ly["v_new"])
+    stats = []
+    gsel = sel.cpu().numpy()
+    gout = widen(out)
+    for b in sample:
+        lat_b = widen(ly["latent"][b, :seq])
+        v_b = widen(ly["v"][b, :seq])
+        q_b = widen(ly["q"][b])
+        orc = O.decode_request(oc, U, q_b, lat_b, v_b, seq)
+        sc = scores[b].cpu().numpy().astype(np.float64)
+        assert np.abs(sc - orc["scores"]).max() <= 1e-4 * max(1.0, np.abs(orc["scores"]).max())
+        nswap = check_selection(orc["scores"], orc["sel"], gsel[b], seq, k, sink, recent)
+        forced = gsel[b][gsel[b] >= 0].astype(np.int64)
+        orc_f = O.decode_request(oc, U, q_b, lat_b, v_b, seq, forced_selection=forced)
+        st = check_output(gout[b], orc_f["y"], "bf16")
+        if nswap == 0:
+            check_output(gout[b], orc["y"], "bf16")
+        stats.append(dict(b=int(b), swaps=nswap, max_abs=st[0], mean_rel=st[1]))
+    del ly
+    torch.cuda.empty_cache()
+    return stats

@@ -157,13 +157,29 @@ def test_graph_capture_replay_is_deterministic():
 
 
 # ------------------------------------------------------------------ full sizes
+@pytest.mark.parametrize("fused", [False, True], ids=["two_calls", "append_decode"])
 @pytest.mark.parametrize("name", ["c2", "c3", "c4"])
-def test_full_size_configs(name):
+def test_full_size_configs(name, fused):
+    """c2-c4 at BASELINE.json's full sizes, every output element against the oracle;
+    ``append_decode`` is the exact call bench.py times (sals_append_decode, bf16 V)."""
     sh = _shape(name)
     s = sh["seq"]
     B = sh["batch"]
-    r = H.full_check(sh, B, [s] * B, seed=synth.SEED_BASE + int(name[1]))
-    print(name, r)
+    r = H.full_check(sh, B, [s] * B, seed=synth.SEED_BASE + int(name[1]) + (100 if fused else 0), fused=fused)
+    print(name, fused, r)
+
+
+@pytest.mark.parametrize("B,n", [(1, 4096), (16, 4096), (64, 4096), (1, 32768), (16, 32768), (64, 32768)])
+def test_c5_grid_points(B, n):
+    """c5 (LLaMA2-7B-shaped MHA 32/32 x 128, r 512, r* 256, k = n/8; BASELINE configs[4],
+    the batched-decode shapes of Table 7 P:705-711 at sparsity 1/8 P:692): one layer in
+    the bench's launch configuration (device-drawn inputs, sals_append_decode); append
+    rows of every request and sampled requests (first, middle, last: the projection's
+    batch passes and the last chunk) element by element against the oracle."""
+    sh = _shape("c5", batch=B, seq=n, top_k=n // 8)
+    sample = sorted({0, B // 2, B - 1})
+    stats = H.sampled_check(sh, B, n, sample=sample, seed=synth.SEED_BASE + 5000 + B + n)
+    print(B, n, stats)
 
 
 def test_full_size_ragged_c3():
@@ -302,15 +318,17 @@ def test_decode_sharded_nccl_one_rank(sink, recent):
 
 
 # ------------------------------------------------------------------ fused append + decode
-@pytest.mark.parametrize("nkv,G,d,B,seqs", [(8, 4, 128, 3, [3000, 1777, 2048]),   # D = 1024: same clusters
+@pytest.mark.parametrize("nkv,G,d,B,seqs", [(8, 4, 128, 3, [3000, 1777, 2048]),   # D = 1024
                                           (32, 1, 128, 2, [4096, 2500])])         # D = 4096
-def test_append_decode_equals_two_calls(nkv, G, d, B, seqs):
-    """sals_append_decode == sals_append_latent(slot s-1) + sals_decode: identical cache
-    rows and selection; outputs equal (D <= 2048: same projection clusters, bit-exact)
-    or within the bf16 output tolerance against the oracle on the same rows."""
+def test_append_decode_against_oracle(nkv, G, d, B, seqs):
+    """sals_append_decode (append + decode in one call) against the oracle, and its
+    cache rows identical to sals_append_latent's (the append writes the same rows
+    whichever call does it; the output is checked against the oracle, never against
+    the other GPU call)."""
     from paper_2510_24273_b200 import sals
     sh = dict(num_q_heads=nkv * G, num_kv_heads=nkv, head_dim=d, rank=256, score_rank=128, top_k=384,
               rope_base=1e6, dtype="bf16")
+    H.full_check(sh, B, seqs, seed=11, fused=True)
     cfg = sals.make_config(**sh)
     p = synth.gen_problem(num_q_heads=nkv * G, num_kv_heads=nkv, head_dim=d, rank=256, batch=B, seq_lens=seqs, seed=11)
     dev = lambda a: torch.from_numpy(a).cuda().bfloat16()
@@ -319,24 +337,12 @@ def test_append_decode_equals_two_calls(nkv, G, d, B, seqs):
     lat2, v2 = lat1.clone(), v1.clone()
     s_max = max(seqs)
     seq = torch.tensor(seqs, dtype=torch.int32, device="cuda")
-    ws1 = sals.alloc_workspace(sals.sals_workspace_bytes(cfg, B, s_max), "cuda")
-    ws2 = sals.alloc_workspace(sals.sals_workspace_bytes(cfg, B, s_max), "cuda")
-    o1 = torch.empty(B, nkv * G * d, dtype=torch.bfloat16, device="cuda")
-    o2 = torch.empty_like(o1)
-    sel1 = torch.full((B, 384), -7, dtype=torch.int32, device="cuda")
-    sel2 = torch.full_like(sel1, -7)
+    ws = sals.alloc_workspace(sals.sals_workspace_bytes(cfg, B, s_max), "cuda")
+    o2 = torch.empty(B, nkv * G * d, dtype=torch.bfloat16, device="cuda")
     sals.sals_append_latent(cfg, U, kn, vn, (seq - 1).to(torch.int32), lat1, v1)
-    sals.sals_decode(cfg, U, q, lat1, v1, seq, s_max, o1, ws1, sel_idx_out=sel1)
-    sals.sals_append_decode(cfg, U, kn, vn, q, lat2, v2, seq, s_max, o2, ws2, sel_idx_out=sel2)
+    sals.sals_append_decode(cfg, U, kn, vn, q, lat2, v2, seq, s_max, o2, ws)
     torch.cuda.synchronize()
     assert torch.equal(lat1, lat2) and torch.equal(v1, v2)
-    if nkv * d <= 2048:
-        assert torch.equal(sel1, sel2) and torch.equal(o1, o2)
-    else:
-        nsame = int((sel1 == sel2).all(dim=1).sum())
-        assert nsame >= B - 1
-        diff = (o1.float() - o2.float()).abs().max().item()
-        assert diff <= 2e-2, diff
 
 
 # ------------------------------------------------------------------ prefill (bulk append)
@@ -409,26 +415,13 @@ def _pack_values(v, bits, nkv):
     return np.concatenate([packed, par], -1).reshape(*lead, -1)
 
 
-def _unpack_values(rows, bits, nkv):
-    """Inverse of _pack_values: the stored codes / scale / zero -> V^ (fp64)."""
-    lead = rows.shape[:-1]
-    r = rows.reshape(*lead, nkv, -1)
-    nb = 128 * bits // 8
-    per = 8 // bits
-    cb = r[..., :nb].astype(np.int64)
-    codes = np.stack([(cb >> (e * bits)) & ((1 << bits) - 1) for e in range(per)], -1).reshape(*lead, nkv, 128)
-    par = np.ascontiguousarray(r[..., nb:nb + 16]).view(np.uint16).reshape(*lead, nkv, 4, 2)
-    to_f = lambda u: torch.from_numpy(u.astype(np.int16)).view(torch.bfloat16).float().numpy().astype(np.float64)
-    scale, zero = to_f(par[..., 0]), to_f(par[..., 1])
-    return O.dequantize_values(codes.reshape(*lead, nkv * 128), scale.reshape(*lead, -1), zero.reshape(*lead, -1), 32)
-
-
 @pytest.mark.parametrize("bits,nkv,G", [(4, 8, 4), (2, 8, 4), (4, 4, 1)])
 def test_quantized_values_decode(bits, nkv, G):
-    """Quantised value cache: the append quantises v_new like the oracle (codes within 1
-    step, identical bf16 parameters in almost every group), and the decode over the
-    stored rows equals the oracle's Algorithm 1 with V replaced by the stored V^
-    (selection in the band, bf16 output tolerances)."""
+    """Quantised value cache: the append's row of the new token is BYTE-identical to the
+    oracle's quantisation of v_new (R15's exact fp32 code rule: codes, bf16 scale and
+    zero), and the decode equals the oracle's Algorithm 1 with V replaced by the
+    oracle's own V^ (O.value_hat of the bf16 values; nothing read back from the GPU
+    cache feeds the oracle): selection in the band, bf16 output tolerances."""
     from paper_2510_24273_b200 import sals
     d, B, seqs, k = 128, 2, [3000, 2311], 384
     D = nkv * d
@@ -451,17 +444,16 @@ def test_quantized_values_decode(bits, nkv, G):
     sals.sals_append_decode(cfg, U, kn, vn, q, lat, vq, seq, s_max, out, ws, sel_idx_out=sel, scores_out=scores)
     torch.cuda.synchronize()
     rows = vq.cpu().numpy()
-    # append: the new token's row vs the oracle's quantisation of v_new
-    for b in range(B):
-        got = rows[b, seqs[b] - 1]
-        ref = _pack_values(H.widen(vn[b:b + 1]), bits, nkv)[0]
-        gv, rv = _unpack_values(got[None], bits, nkv)[0], _unpack_values(ref[None], bits, nkv)[0]
-        _, sc_ref, _ = O.quantize_values(H.widen(vn[b:b + 1]), bits, 32)
-        assert np.all(np.abs(gv - rv) <= sc_ref.repeat(32, -1)[0] * 1.01 + 1e-6)
-    # decode vs the oracle over the stored V^ (cache mode)
-    vhat = _unpack_values(rows, bits, nkv)
+    vn_host = H.widen(vn)
+    v_full = v_host.copy()
+    for b in range(B):   # append: the new token's row, byte for byte
+        np.testing.assert_array_equal(rows[b, seqs[b] - 1], _pack_values(vn_host[b:b + 1], bits, nkv)[0])
+        v_full[b, seqs[b] - 1] = vn_host[b]
     oc = H.oracle_cfg(sh)
     host_lat = H.widen(lat)
+    vhat = np.zeros_like(v_full)
+    for b in range(B):
+        vhat[b, :seqs[b]] = O.value_hat(v_full[b], bits, 0, seqs[b])
     orc = O.decode(oc, H.widen(U), H.widen(q), host_lat, vhat, np.array(seqs))
     forced = []
     for b in range(B):
@@ -483,15 +475,6 @@ def _pack8(v, nkv):
     return np.concatenate([c, par], -1).reshape(*lead, -1)
 
 
-def _unpack8(rows, nkv):
-    lead = rows.shape[:-1]
-    r = rows.reshape(*lead, nkv, 144)
-    codes = r[..., :128].astype(np.int64).reshape(*lead, nkv * 128)
-    par = np.ascontiguousarray(r[..., 128:]).view(np.uint16).reshape(*lead, nkv, 4, 2)
-    to_f = lambda u: torch.from_numpy(u.astype(np.int16)).view(torch.bfloat16).float().numpy().astype(np.float64)
-    return O.dequantize_values(codes, to_f(par[..., 0]).reshape(*lead, -1), to_f(par[..., 1]).reshape(*lead, -1), 32)
-
-
 @pytest.mark.parametrize("bits,nkv,G,z", [(4, 8, 4, 64), (2, 4, 1, 100), (4, 8, 2, 20), (2, 8, 4, 128)])
 def test_quantized_values_recent_window(bits, nkv, G, z):
     """Quantised values with the high-precision recent window: the forced
@@ -507,6 +490,10 @@ def test_quantized_values_recent_window_c3_size():
 
 
 def _quantized_window_case(bits, nkv, G, z, seqs, k, rank, rstar, seed):
+    """The cache holds the oracle's b-bit rows and 8-bit recent-window ring for the old
+    tokens; the append writes the new token's b-bit row and ring slot, which must be
+    byte-identical to the oracle's; the decode is compared with the oracle's
+    Algorithm 1 over O.value_hat (mixed precision V^) of the bf16 values."""
     from paper_2510_24273_b200 import sals
     d, B = 128, len(seqs)
     sh = dict(num_q_heads=nkv * G, num_kv_heads=nkv, head_dim=d, rank=rank, score_rank=rstar, top_k=k,
@@ -524,7 +511,7 @@ def _quantized_window_case(bits, nkv, G, z, seqs, k, rank, rstar, seed):
     main = _pack_values(v_host, bits, nkv)                               # [B, cap, rb]
     ring = np.zeros((B, z, nkv * 144), dtype=np.uint8)
     for b in range(B):
-        for pos in range(seqs[b] - z, seqs[b]):
+        for pos in range(seqs[b] - z, seqs[b] - 1):                      # the new token's slot: the append's
             ring[b, pos % z] = _pack8(v_host[b, pos][None], nkv)[0]
     vq = torch.from_numpy(np.concatenate([main.reshape(-1), ring.reshape(-1)])).cuda()
     seq = torch.tensor(seqs, dtype=torch.int32, device="cuda")
@@ -536,16 +523,16 @@ def _quantized_window_case(bits, nkv, G, z, seqs, k, rank, rstar, seed):
     allb = vq.cpu().numpy()
     rows = allb[:B * cap * rb].reshape(B, cap, rb)
     ringg = allb[B * cap * rb:].reshape(B, z, nkv * 144)
-    vhat = _unpack_values(rows, bits, nkv)
+    vn_host = H.widen(vn)
+    v_full = v_host.copy()
     for b in range(B):
         s = seqs[b]
-        # the append's 8-bit row of the new token vs the oracle quantiser (one code step)
-        _, sc8, _ = O.quantize_values(H.widen(vn[b:b + 1]), 8, 32)
-        got8 = _unpack8(ringg[b, (s - 1) % z][None], nkv)[0]
-        ref8 = _unpack8(_pack8(H.widen(vn[b:b + 1]), nkv), nkv)[0]
-        assert np.all(np.abs(got8 - ref8) <= sc8.repeat(32, -1)[0] * 1.01 + 1e-6)
-        for pos in range(s - z, s):
-            vhat[b, pos] = _unpack8(ringg[b, pos % z][None], nkv)[0]
+        np.testing.assert_array_equal(rows[b, s - 1], _pack_values(vn_host[b:b + 1], bits, nkv)[0])
+        np.testing.assert_array_equal(ringg[b, (s - 1) % z], _pack8(vn_host[b:b + 1], nkv)[0])
+        v_full[b, s - 1] = vn_host[b]
+    vhat = np.zeros_like(v_full)
+    for b in range(B):
+        vhat[b, :seqs[b]] = O.value_hat(v_full[b], bits, z, seqs[b])
     oc = H.oracle_cfg(sh, recent=z)
     host_lat = H.widen(lat)
     orc = O.decode(oc, H.widen(U), H.widen(q), host_lat, vhat, np.array(seqs))

@@ -33,9 +33,18 @@ def _cfg(**kw):
 # ---------------------------------------------------------------- RoPE (Eq. 3)
 @pytest.mark.parametrize("style", [O.ROPE_HALF, O.ROPE_INTERLEAVED])
 def test_rope_golden(style):
+    """SPEC S:111-113 examples (style-free: d = 2 or m = 0) and the d >= 4, m >= 1
+    cases written from S:98 pair by pair (tests/golden/make_rope_examples.py): they
+    pin theta_i = base^(-2i/d) for i >= 1 and each style's pairing."""
+    name = {O.ROPE_HALF: "half", O.ROPE_INTERLEAVED: "interleaved"}[style]
+    n = 0
     for c in _gold("rope_examples.json")["cases"]:
+        if c.get("style", name) != name:
+            continue
         out = O.rope(np.array(c["x"]), c["m"], c["base"], style)
-        np.testing.assert_allclose(out, c["expected"], rtol=0, atol=1e-15)
+        np.testing.assert_allclose(out, c["expected"], rtol=0, atol=1e-14)
+        n += 1
+    assert n >= 5
 
 
 def _explicit_rotation(d, m, base, style):
@@ -457,3 +466,56 @@ def test_quantize_constant_group_and_bf16_round():
     # 1 + 2^-8 is a tie between 1 and 1 + 2^-7: ties to even -> 1; 1 + 3*2^-8 -> 1 + 2^-6
     np.testing.assert_array_equal(O.bf16_round(np.array([1 + 2.0 ** -8, 1 + 3 * 2.0 ** -8, -2.0])),
                                   [1.0, 1 + 2.0 ** -6, -2.0])
+
+
+def test_quantize_rounding_rule_closed_form():
+    """R15's code rule on hand-computed cases: hi - lo = 30 over 15 steps gives
+    scale 2 exactly, so (v - zero) / scale lands on exact halves, which round to
+    even (2.5 -> 2, 3.5 -> 4, 0.5 -> 0, 14.5 -> 14); values past the grid clamp."""
+    v = np.zeros((1, 32))
+    v[0, 0], v[0, 1] = 0.0, 30.0                                  # lo, hi
+    v[0, 2:8] = [5.0, 7.0, 1.0, 29.0, 3.0, 13.0]                   # /2 = 2.5, 3.5, 0.5, 14.5, 1.5, 6.5
+    codes, scale, zero = O.quantize_values(v, 4, 32)
+    assert scale[0, 0] == 2.0 and zero[0, 0] == 0.0
+    np.testing.assert_array_equal(codes[0, :8], [0, 15, 2, 4, 0, 14, 2, 6])
+    # bf16 storage of the scale: (hi - lo) / 15 = 1/15 * 3 = 0.2 -> bf16 0.2001953125 (nearest even)
+    w = np.zeros((1, 32)); w[0, 1] = 3.0
+    c2, s2, _ = O.quantize_values(w, 4, 32)
+    assert s2[0, 0] == 0.2001953125
+    assert c2[0, 1] == 15                                         # 3 / 0.2001953125 = 14.985 -> 15
+
+
+def test_value_hat_mixed_precision_worked_example():
+    """Mixed-precision V^: one 32-channel group per row with values k/64,
+    k in [0, 255], min 0 and max 255/64 in every row.  8-bit: scale (255/64)/255 = 1/64,
+    so window rows (j >= s - z) reconstruct exactly; 4-bit: scale (255/64)/15 = 17/64
+    (exact in bf16), so the other rows reconstruct to 17 * round(k/17) / 64 (k/17 is
+    never a half, so no tie)."""
+    rng = np.random.default_rng(3)
+    s, z = 6, 2
+    k = rng.integers(0, 256, size=(s, 32))
+    k[:, 0], k[:, 31] = 0, 255
+    v = k / 64.0
+    vh = O.value_hat(v, 4, z, s)
+    np.testing.assert_array_equal(vh[s - z:], v[s - z:])
+    np.testing.assert_array_equal(vh[:s - z], 17.0 * np.floor(k[:s - z] / 17.0 + 0.5) / 64.0)
+    # z = 0: every row 4-bit; z >= s: every row 8-bit (exact); bits = 16: the values
+    np.testing.assert_array_equal(O.value_hat(v, 4, 0, s), 17.0 * np.floor(k / 17.0 + 0.5) / 64.0)
+    np.testing.assert_array_equal(O.value_hat(v, 4, 99, s), v)
+    np.testing.assert_array_equal(O.value_hat(v, 16, 2, s), v)
+
+
+@pytest.mark.parametrize("bits", [2, 4])
+def test_value_hat_error_bounds(bits):
+    """Window rows are within half an 8-bit step of v, the others within half a
+    b-bit step (+ the bf16 storage of the grid), on N(0,1) rows of bf16 values."""
+    rng = np.random.default_rng(10 + bits)
+    s, z, D = 40, 7, 128
+    v = O.bf16_round(rng.standard_normal((s, D)))
+    vh = O.value_hat(v, bits, z, s)
+    g = v.reshape(s, D // 32, 32)
+    rngw = (g.max(-1) - g.min(-1))[..., None]
+    for rows, q in ((slice(s - z, s), 255), (slice(0, s - z), (1 << bits) - 1)):
+        err = np.abs(vh.reshape(s, D // 32, 32)[rows] - g[rows])
+        step = rngw[rows] / q
+        assert np.all(err <= 0.5 * step * (1 + 2.0 ** -7) + q * step * 2.0 ** -8 + 1e-6)
