@@ -45,7 +45,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["sals", "reference"], default="sals")
-    ap.add_argument("--workload", choices=["c2", "c3", "c4", "c4-sharded", "c5"], default="c2")
+    ap.add_argument("--workload", choices=["all", "c2", "c3", "c4", "c4-sharded", "c5"], default="all",
+                    help="all (default): c2 is the headline line (BASELINE configs[1], the metric's 4K point), "
+                         "c3 (32K) and c4 (128K) are measured the same way and reported under 'workloads'")
     ap.add_argument("--sweep-batches", default="1,2,4,8,16,32,64")
     ap.add_argument("--sweep-seqs", default="4096,8192,16384,32768")
     ap.add_argument("--layers", type=int, default=32)
@@ -75,6 +77,8 @@ def load_peaks():
 
 
 def workload_shape(name):
+    if name == "all":   # the headline line's workload
+        name = "c2"
     base = "c4" if name.startswith("c4") else name
     sh = dict(synth.CONFIGS[base])
     if base == "c5":   # single-point uses (the reference arm): the sweep's B = 8, n = 4K point
@@ -194,12 +198,33 @@ def oracle_step(cfg, p, s):
     return time.perf_counter() - t0
 
 
-def oracle_sample(sh, budget_s=12.0):
+def oracle_sample(sh, budget_s=12.0, threads=None):
+    """Median seconds of one request x one layer through the oracle (as it stands), for
+    ~budget_s of CPU time; ``threads`` limits the BLAS pool (1 = the single-core figure)."""
     cfg, p = oracle_problem(sh)
-    times, t_all = [], time.perf_counter()
-    while not times or time.perf_counter() - t_all < budget_s:
-        times.append(oracle_step(cfg, p, sh["seq"]))
-    return float(np.median(times)), len(times), oracle_cores()
+    from contextlib import nullcontext
+    try:
+        from threadpoolctl import threadpool_limits
+        ctx = threadpool_limits(threads) if threads else nullcontext()
+    except Exception:
+        ctx = nullcontext()
+    with ctx:
+        times, t_all = [], time.perf_counter()
+        while not times or time.perf_counter() - t_all < budget_s:
+            times.append(oracle_step(cfg, p, sh["seq"]))
+        cores = threads or oracle_cores()
+    return float(np.median(times)), len(times), cores
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
 
 def run_reference(args, rank, world):
@@ -262,9 +287,26 @@ def time_graph(g, stream, steps, warmup, world):
     return e0.elapsed_time(e1) / steps
 
 
-def run_sals(args, rank, world):
+PAPER_CONTEXT = {
+    "note": "the paper's own figures on its own hardware (context only, not comparable and not a target): "
+            "'one GPU (ampere architecture)', Xeon Platinum 8336C, 128G RAM (P:481); Triton fused kernel on "
+            "PyTorch (P:689)",
+    "attention_operator_speedup_vs_flashattention2_4k": {"claimed": 5.7, "cite": "P:31 (abstract / contributions)"},
+    "table6_bs8_4k_ms": {"flash_attn2": 1.630, "sals_25pct": 0.530, "sals_12_5pct": 0.439,
+                         "ratios": [round(1.630 / 0.530, 2), round(1.630 / 0.439, 2)],
+                         "cite": "Table 6, P:664-672 (the text's '7,46x' at P:698 disagrees with the table; R11)"},
+    "e2e_vs_gpt_fast": {"claimed": [1.4, 4.5], "cite": "P:31; Table 7 P:705-711",
+                        "table7_tokens_per_s": {"bs8_4k": {"gpt_fast": 118, "sals_25pct": 154.1, "sals_12_5pct": 163.5},
+                                                "bs8_32k": {"gpt_fast": 19.8, "sals_25pct": 67.97,
+                                                            "sals_12_5pct": 89.47}}},
+}
+
+
+def measure(args, workload, rank, world, with_e2e=True):
+    """One workload (c2 / c3 / c4): the 32-layer step timed as a CUDA-graph replay, live
+    per-stage times, the dense comparator, e2e through the public API, the roofline."""
     from paper_2510_24273_b200 import sals, traffic
-    base, sh = workload_shape(args.workload)
+    base, sh = workload_shape(workload)
     L, B, s = args.layers, sh["batch"], sh["seq"]
     dev = "cuda"
     pol = policy_of(args.policy, base, L)
@@ -287,7 +329,7 @@ def run_sals(args, rank, world):
                 ring[..., 128:] = par8
             ly["vq"] = buf
     vkey = "vq" if args.v_bits else "v"
-    D, nqd = sh["num_kv_heads"] * sh["head_dim"], sh["num_q_heads"] * sh["head_dim"]
+    nqd = sh["num_q_heads"] * sh["head_dim"]
     seq = torch.full((B,), s, dtype=torch.int32, device=dev)
     pos = seq - 1
     ws = sals.alloc_workspace(sals.sals_workspace_bytes(cfg, B, s), dev)
@@ -353,18 +395,18 @@ def run_sals(args, rank, world):
         dense = {"ms_per_step": dms, "tokens_per_s": world * B / (dms / 1e3),
                  "hbm_frac_of_measured": (dbytes * L / (dms / 1e3)) / (peaks["hbm_gbs"] * 1e9),
                  "kernel": "in-build split-K flash decode over the full post-RoPE K/V cache"}
+        del gd, wsd
 
     # ---- e2e through the public API with host buffers
-    e2e = run_e2e(cfg, layers, seq, pos, s, ws, out, stream, args, world, pol, wsd_pol, cfg_dense, vkey)
+    e2e = run_e2e(cfg, layers, seq, pos, s, ws, out, stream, args, world, pol, wsd_pol, cfg_dense, vkey) \
+        if with_e2e else None
 
     # ---- roofline of the dominant kernel
     peaks, peak_kind = load_peaks()
-    roof = roofline(sh, stages, peaks, peak_kind, args.workload, sals.sals_v_row_bytes(cfg) if args.v_bits else None)
-    line = {
-        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": describe(args.workload, sh, L), "batch": B, "seq_len": s, "layers": L,
+    roof = roofline(sh, stages, peaks, peak_kind, sals.sals_v_row_bytes(cfg) if args.v_bits else None)
+    res = {
+        "value": value, "ms_per_step": ms, "B": B,
+        "config": {"workload": describe(workload, sh, L), "batch": B, "seq_len": s, "layers": L,
                    "l2": "inputs larger than L2: 32 distinct layers' caches per step",
                    "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
         "us_per_layer_step": ms * 1e3 / L,
@@ -379,16 +421,70 @@ def run_sals(args, rank, world):
         "launches_per_step": int(launches_per_step),
         "clocks": clk.summary(),
         "e2e": e2e,
+        "dense": dense,
+        "speedup_vs_dense": (dense["ms_per_step"] / ms) if dense else None,
+        "sh": sh,
     }
-    if dense:
-        line["dense"] = dense
-        line["speedup_vs_dense"] = dense["ms_per_step"] / ms
+    del layers, g, ws, out
+    torch.cuda.empty_cache()
+    return res
+
+
+def summary_of(w, r):
+    """Per-workload entry of the default line's 'workloads' object."""
+    roof = r["roofline"] or {}
+    fr = {roof.get("kernel"): roof.get("frac")} if roof else {}
+    fr.update({k: v.get("frac") for k, v in (roof.get("others") or {}).items()})
+    return {
+        "workload": r["config"]["workload"],
+        "us_per_layer_step": round(r["us_per_layer_step"], 2),
+        "tokens_per_s": round(r["value"], 1),
+        "e2e_tokens_per_s": round(r["e2e"]["value"], 1) if r["e2e"] else None,
+        "vs_dense": round(r["speedup_vs_dense"], 3) if r["speedup_vs_dense"] else None,
+        "dense_us_per_layer_step": round(r["dense"]["ms_per_step"] * 1e3 / r["config"]["layers"], 2) if r["dense"] else None,
+        "dense_hbm_frac_of_measured": round(r["dense"]["hbm_frac_of_measured"], 3) if r["dense"] else None,
+        "stages_us": r["stages_us"],
+        "stage_sum_us": round(sum(r["stages_us"].values()), 2),
+        "roofline_frac": {k: (round(v, 3) if v is not None else None) for k, v in fr.items()},
+        "recon_attn_hbm_frac": round(roof["hbm_frac"], 3) if roof.get("kernel") == "recon_attn" else
+        (round(roof["others"]["recon_attn"]["hbm_frac"], 3) if "recon_attn" in (roof.get("others") or {}) else None),
+        "clocks": r["clocks"],
+    }
+
+
+def run_sals(args, rank, world):
+    names = ["c2", "c3", "c4"] if args.workload == "all" else [args.workload]
+    res = {}
+    for w in names:
+        res[w] = measure(args, w, rank, world, with_e2e=True)
+    head_name = names[0]
+    r = res[head_name]
+    sh, L, B = r["sh"], args.layers, r["B"]
+    line = {
+        "metric": METRIC, "value": r["value"], "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": r["config"],
+    }
+    for k in ("us_per_layer_step", "stages_us", "path", "policy", "v_bits", "api", "roofline", "gpu_launches",
+              "launches_per_step", "clocks", "e2e"):
+        line[k] = r[k]
+    if r["dense"]:
+        line["dense"] = r["dense"]
+        line["speedup_vs_dense"] = r["speedup_vs_dense"]
+    if len(names) > 1:
+        line["workloads"] = {w: summary_of(w, res[w]) for w in names}
+        line["gpu_launches_all_workloads"] = sum(res[w]["gpu_launches"] for w in names)
+    line["paper_context"] = PAPER_CONTEXT
     if rank == 0 and not args.no_cpu_baseline:
         t_req, n, cores = oracle_sample(sh, budget_s=12.0)
-        v = 1.0 / (t_req * L)
-        line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "oracle",
-                                "sample": f"{n} single-request x single-layer oracle decodes at the full workload "
-                                          f"shape (median {t_req:.3f} s), extrapolated x{B} requests x{L} layers"}
+        t1, n1, _ = oracle_sample(sh, budget_s=8.0, threads=1)
+        line["cpu_baseline"] = {"value": 1.0 / (t_req * L), "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                                "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+                                "sample": f"{n} single-request x single-layer oracle decodes at the full {head_name} "
+                                          f"shape (median {t_req:.3f} s), extrapolated x{B} requests x{L} layers",
+                                "one_core": {"value": 1.0 / (t1 * L), "unit": "tokens/s", "cores": 1,
+                                             "sample": f"{n1} decodes, BLAS limited to 1 thread (median {t1:.3f} s)"}}
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -422,49 +518,68 @@ def run_sweep(args, rank, world):
     holds 32 distinct layers in HBM (layer 0 drawn with the synth recipe, layers
     1..31 device copies of it: distinct memory, so every step streams all 32
     layers' caches) and is timed as a CUDA-graph replay like the single-config
-    lines.  Points whose caches do not fit in ~0.9 x HBM are reported as such."""
+    lines.  ``--policy paper`` applies the paper's serving policy to every point
+    (sink / recent 16 / 64 forced, layers {0, 1, 31} dense through
+    the in-build dense kernels).  A point is reported as not
+    fitting when its resident caches (32 layers) plus one request's fp32 draw
+    temporaries exceed the free device memory less 2 GiB."""
     from paper_2510_24273_b200 import sals
     base = dict(synth.CONFIGS["c5"])
     L = args.layers
     D = base["num_kv_heads"] * base["head_dim"]
-    budget = 0.88 * torch.cuda.get_device_properties(0).total_memory
+    r = base["rank"]
     rows = []
     stream = torch.cuda.Stream()
+    pol = policy_of(args.policy, "c5", L)
 
-    def make_layers(sh, dense):
+    def make_layers(sh, dense_layers, sals_layers):
         g = torch.Generator(device="cuda")
         g.manual_seed(synth.SEED_BASE + 5000 + 1000 * rank)
         l0 = synth.gen_layer_torch(num_q_heads=sh["num_q_heads"], num_kv_heads=sh["num_kv_heads"],
                                    head_dim=sh["head_dim"], rank=sh["rank"], batch=sh["batch"], seq=sh["seq"],
-                                   generator=g, device="cuda", dense=dense)
-        if dense:
-            l0.pop("latent")
-        out = [l0]
-        for _ in range(L - 1):
-            out.append({k: v.clone() for k, v in l0.items()})
+                                   generator=g, device="cuda", dense=bool(dense_layers))
+        out = []
+        for l in range(L):
+            keep = {k: v for k, v in l0.items()
+                    if (k != "k_dense" or l in dense_layers) and (k != "latent" or l in sals_layers)}
+            out.append(keep if l == 0 else {k: v.clone() for k, v in keep.items()})
+        if 0 not in dense_layers:
+            l0.pop("k_dense", None)
         return out
+
+    def fits(B, n, per_layer_elems, n_layers):
+        free = torch.cuda.mem_get_info()[0] - 2 * 2 ** 30
+        need = n_layers * per_layer_elems * 2 + B * n * 4 * 2 * D     # + a request's fp32 draws (generous)
+        return need <= free
 
     for n in [int(x) for x in args.sweep_seqs.split(",")]:
         for B in [int(x) for x in args.sweep_batches.split(",")]:
             sh = dict(base, batch=B, seq=n, top_k=n // 8)
             row = {"batch": B, "seq": n, "top_k": n // 8}
-            cfg = sals.make_config(**sh)
+            cfg = sals.make_config(**sh, sink=pol["sink"], recent=pol["recent"])
+            cfg_dense = sals.make_config(**sh)
             seq = torch.full((B,), n, dtype=torch.int32, device="cuda")
             pos = seq - 1
             nqd = sh["num_q_heads"] * sh["head_dim"]
             out = torch.empty(L, B, nqd, dtype=torch.bfloat16, device="cuda")
-            # ---- SALS
-            need = L * B * n * (sh["rank"] + D) * 2 + 2 * B * n * D * 4
-            if need > budget:
+            dl = set(pol["dense_layers"])
+            sl = set(range(L)) - dl
+            # ---- SALS (with the policy's dense layers)
+            if not fits(B, n, B * n * (len(sl) * (r + D) + len(dl) * 2 * D) / L, L):
                 row["sals"] = "does not fit"
             else:
-                layers = make_layers(sh, False)
+                layers = make_layers(sh, dl, sl)
                 ws = sals.alloc_workspace(sals.sals_workspace_bytes(cfg, B, n), "cuda")
+                wsd = sals.alloc_workspace(sals.sals_dense_workspace_bytes(cfg_dense, B, n), "cuda") if dl else None
 
                 def step():
                     for l, ly in enumerate(layers):
-                        sals.sals_append_decode(cfg, ly["U"], ly["k_new"], ly["v_new"], ly["q"], ly["latent"], ly["v"],
-                                                seq, n, out[l], ws)
+                        if l in dl:
+                            sals.sals_dense_append(cfg_dense, ly["k_new"], ly["v_new"], pos, ly["k_dense"], ly["v"])
+                            sals.sals_dense_decode(cfg_dense, ly["q"], ly["k_dense"], ly["v"], seq, n, out[l], wsd)
+                        else:
+                            sals.sals_append_decode(cfg, ly["U"], ly["k_new"], ly["v_new"], ly["q"], ly["latent"],
+                                                    ly["v"], seq, n, out[l], ws)
                 with torch.cuda.stream(stream):
                     step()
                     stream.synchronize()
@@ -474,20 +589,19 @@ def run_sweep(args, rank, world):
                     ms = max_over_ranks(time_graph(gr, stream, args.steps, args.warmup, world), world)
                 row["sals_ms_per_step"] = ms
                 row["sals_tokens_per_s"] = world * B / (ms / 1e3)
-                del gr, layers, ws
+                del gr, layers, ws, wsd
                 torch.cuda.empty_cache()
-            # ---- dense comparator
-            need = L * B * n * 2 * D * 2 + 2 * B * n * D * 4
-            if need > budget:
+            # ---- dense comparator (every layer dense)
+            if not fits(B, n, B * n * 2 * D, L):
                 row["dense"] = "does not fit"
             else:
-                layers = make_layers(sh, True)
-                wsd = sals.alloc_workspace(sals.sals_dense_workspace_bytes(cfg, B, n), "cuda")
+                layers = make_layers(sh, set(range(L)), set())
+                wsd = sals.alloc_workspace(sals.sals_dense_workspace_bytes(cfg_dense, B, n), "cuda")
 
                 def dstep():
                     for l, ly in enumerate(layers):
-                        sals.sals_dense_append(cfg, ly["k_new"], ly["v_new"], pos, ly["k_dense"], ly["v"])
-                        sals.sals_dense_decode(cfg, ly["q"], ly["k_dense"], ly["v"], seq, n, out[l], wsd)
+                        sals.sals_dense_append(cfg_dense, ly["k_new"], ly["v_new"], pos, ly["k_dense"], ly["v"])
+                        sals.sals_dense_decode(cfg_dense, ly["q"], ly["k_dense"], ly["v"], seq, n, out[l], wsd)
                 with torch.cuda.stream(stream):
                     dstep()
                     stream.synchronize()
@@ -514,6 +628,7 @@ def run_sweep(args, rank, world):
                                f"value = the highest-throughput point (B={head['batch']}, n={head['seq']})" if head else "c5",
                    "l2": "inputs larger than L2: 32 distinct layers' caches per step",
                    "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "policy": {k: (list(v) if isinstance(v, tuple) else v) for k, v in pol.items()},
         "sweep": rows,
     }
     if rank == 0:
@@ -564,7 +679,7 @@ def run_e2e(cfg, layers, seq, pos, s, ws, out, stream, args, world, pol=None, ws
                    "stream sync per step"}
 
 
-def roofline(sh, stages, peaks, peak_kind, workload, v_row_bytes=None):
+def roofline(sh, stages, peaks, peak_kind, v_row_bytes=None):
     from paper_2510_24273_b200 import traffic
     B, s = sh["batch"], sh["seq"]
     kw = dict(batch=B, seq=s, num_q_heads=sh["num_q_heads"], num_kv_heads=sh["num_kv_heads"],
@@ -589,18 +704,11 @@ def roofline(sh, stages, peaks, peak_kind, workload, v_row_bytes=None):
     r = dict(cand[dom])
     r["kernel"] = dom
     r["peak_source"] = f"{peak_kind} (MEASURED_PEAKS.json burst)" if peak_kind == "measured" else "fallback"
-    r["traffic"] = ncu_traffic(workload, dom)
+    # DRAM bytes are not measured inside this run (no profiler in a timed bench); the
+    # ncu dram__bytes per launch of the same kernels is in profiles/r2/ 
+    r["traffic"] = None
     r["others"] = {k: {kk: v[kk] for kk in ("bound", "achieved", "unit", "frac")} for k, v in cand.items() if k != dom}
     return r
-
-
-def ncu_traffic(workload, kernel):
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if not os.path.exists(p):
-        return None
-    with open(p) as f:
-        d = json.load(f)
-    return d.get(workload, {}).get(kernel)
 
 
 def main():

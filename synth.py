@@ -113,7 +113,11 @@ def gen_layer_torch(*, num_q_heads, num_kv_heads, head_dim, rank, batch, seq, ca
     U, _ = torch.linalg.qr(torch.randn(D, rank, device=device, generator=g, dtype=torch.float32))
     sig = torch.tensor(spectrum(rank), device=device, dtype=torch.float32)
     c = float(np.sqrt(D / float((sig ** 2).sum())))
-    latent = torch.randn(batch, cap, rank, device=device, generator=g, dtype=torch.float32) * (c * sig)
+    # per-request draws (fp32 temporaries of one request at a time: bench-sized batches
+    # of 32 layers fill most of HBM)
+    latent = torch.empty(batch, cap, rank, device=device, dtype=dtype)
+    for b in range(batch):
+        latent[b] = (torch.randn(cap, rank, device=device, generator=g, dtype=torch.float32) * (c * sig)).to(dtype)
     w = torch.randn(rank, device=device, generator=g) * sig
     u = (U @ w).view(num_kv_heads, head_dim)
     u = u / u.norm(dim=1, keepdim=True)
@@ -122,16 +126,24 @@ def gen_layer_torch(*, num_q_heads, num_kv_heads, head_dim, rank, batch, seq, ca
     n = max(1, seq // 64)
     pos = torch.randint(0, max(seq - 1, 1), (batch, n), device=device, generator=g)
     amp = 3.0 * c * float(sig.norm())
-    latent.scatter_add_(1, pos[..., None].expand(batch, n, rank),
-                        (amp * w / w.norm()).expand(batch, n, rank).contiguous())
+    hit = (amp * w / w.norm())
+    for b in range(batch):   # planted heavy hitters (fp32 add, one rounding to the storage type)
+        rows = latent[b, pos[b]].float() + hit
+        latent[b, pos[b]] = rows.to(dtype)
+    v = torch.empty(batch, cap, D, device=device, dtype=dtype)
+    for b in range(batch):
+        v[b] = torch.randn(cap, D, device=device, generator=g, dtype=torch.float32).to(dtype)
     out = {
         "U": U.to(dtype).contiguous(),
-        "latent": latent.to(dtype),
-        "v": torch.randn(batch, cap, D, device=device, generator=g, dtype=torch.float32).to(dtype),
+        "latent": latent,
+        "v": v,
         "q": q.reshape(batch, num_q_heads * head_dim).to(dtype),
         "k_new": torch.randn(batch, D, device=device, generator=g).to(dtype),
         "v_new": torch.randn(batch, D, device=device, generator=g).to(dtype),
     }
     if dense:   # dense comparator's key cache: independent N(0,1) draws (timing only)
-        out["k_dense"] = torch.randn(batch, cap, D, device=device, generator=g, dtype=torch.float32).to(dtype)
+        kd = torch.empty(batch, cap, D, device=device, dtype=dtype)
+        for b in range(batch):
+            kd[b] = torch.randn(cap, D, device=device, generator=g, dtype=torch.float32).to(dtype)
+        out["k_dense"] = kd
     return out
