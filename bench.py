@@ -351,6 +351,10 @@ def measure(args, workload, rank, world, with_e2e=True):
                                         seq, s, out[l], ws)
 
     stream = torch.cuda.Stream()
+    # the synthetic layers, seq / pos and the workspace were made on the default stream:
+    # finish that work before the first call on the side stream (a cross-stream race
+    # otherwise lets the first step read half-written seq_len / caches)
+    torch.cuda.synchronize()
     with torch.cuda.stream(stream):
         step()                                 # eager warm-up (sets kernel attributes)
         stream.synchronize()
@@ -580,6 +584,7 @@ def run_sweep(args, rank, world):
                         else:
                             sals.sals_append_decode(cfg, ly["U"], ly["k_new"], ly["v_new"], ly["q"], ly["latent"],
                                                     ly["v"], seq, n, out[l], ws)
+                torch.cuda.synchronize()   # layers / seq were made on the default stream
                 with torch.cuda.stream(stream):
                     step()
                     stream.synchronize()
@@ -602,6 +607,7 @@ def run_sweep(args, rank, world):
                     for l, ly in enumerate(layers):
                         sals.sals_dense_append(cfg_dense, ly["k_new"], ly["v_new"], pos, ly["k_dense"], ly["v"])
                         sals.sals_dense_decode(cfg_dense, ly["q"], ly["k_dense"], ly["v"], seq, n, out[l], wsd)
+                torch.cuda.synchronize()
                 with torch.cuda.stream(stream):
                     dstep()
                     stream.synchronize()

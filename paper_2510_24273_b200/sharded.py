@@ -138,6 +138,7 @@ def bench(args, rank, world):
 
     stream = torch.cuda.Stream()
     graph = None
+    torch.cuda.synchronize()   # inputs were made on the default stream
     with torch.cuda.stream(stream):
         step()
         stream.synchronize()
