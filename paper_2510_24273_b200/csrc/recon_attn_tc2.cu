@@ -300,6 +300,7 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
   }
   if (tid == 0) TSTAMP(80);
   pdl_wait();
+  if (tid == 0) TSTAMP(82);
   const int cnt = a.count[b];
   const int ntiles_b = (cnt + kRows - 1) / kRows;
   const int t_begin = chunk * a.tiles_per_cta;
@@ -469,7 +470,9 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
           cp_async_16(base + rl * 128 + ((ch ^ (rl & 7)) << 4), src, row >= 0 ? 16u : 0u);
         }
         cp_async_arrive_noinc(&full[s]);
+        if (aw == 0 && lane == 0 && kc == 0) TSTAMP(64 + it);
       }
+      if (aw == 0 && lane == 0) TSTAMP(72 + it);
 #pragma unroll
       for (int i = 0; i < 8; ++i) rows[i] = rows_nx[i];
     }
