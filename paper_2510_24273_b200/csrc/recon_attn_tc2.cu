@@ -41,7 +41,7 @@ static_assert(1024 + 3 * (128 * 64 * 2 + 256 * 64 * 2) + 128 * 256 * 2 + 8 * 64 
                   232448, "G = 4 shared memory over the 227 KB limit");
 __host__ __device__ constexpr int smem_bytes(int G) {
   return 1024 + kStages * (kABytes + kBBytes) + kVBytes + 2 * G * 64 * 8 /*sQ*/ + 2 * 2 * G * kRows * 4 /*sL*/ +
-         2 * G * kPS * 4 /*sP*/ + 1024 /*misc: sRed, sAl, sIdxV, barriers, TMEM slot (< 1 KB)*/;
+         (2 * G * kPS * 4 > 4096 ? 2 * G * kPS * 4 : 4096) /*sP*/ + 1024 /*misc: sRed, sAl, sIdxV, barriers, TMEM slot (< 1 KB)*/;
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -157,6 +157,40 @@ __device__ __forceinline__ void tmem_ldn_nowait(uint32_t taddr, float* v) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// P V on tcgen05 (bf16 values): A = the staged V tile as an MN-major SWIZZLE_128B
+// operand (M = 128 dims of one KV head, K = 16 tokens per instruction: 64-dim blocks
+// LBO = 16 KB apart, 8-token row groups SBO = 1 KB apart), B = P^T as a K-major
+// SWIZZLE_128B operand (N = 8 rows = query heads, K = tokens), D = O_tile^T in TMEM
+// (lane = dim, column = query head), fp32.
+__device__ __forceinline__ uint64_t sw128_mn_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)(16384 >> 4) << 16;   // LBO: next 64-element block along M
+  d |= (uint64_t)(1024 >> 4) << 32;    // SBO: next 8-row group along K
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+constexpr uint32_t kIdescPV = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) /*A MN-major*/ | ((uint32_t)(8 >> 3) << 17) |
+                              ((uint32_t)(128 >> 4) << 24);
+__device__ __forceinline__ void mma_bf16_pv(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdescPV), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
+
 struct KArgs {
   TcArgs a;
 };
@@ -236,6 +270,13 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
   constexpr int NQH = 2 * G;             // query heads of this CTA (2 KV heads)
   constexpr int VB = VBH >= 20 ? VBH / 10 : VBH;
   constexpr bool HPW = VBH >= 20;        // recent-window variant
+  // bf16 values with GQA (G >= 2): P V on tcgen05 (P rounded to bf16, fp32 accumulation
+  // in TMEM), issued by the MMA warp between the reconstruction chunks of the next tile.
+  // MHA (G = 1: 1 FFMA2 per token and dim pair) and quantised values (dequantisation in
+  // the loop) keep the CUDA-core P V over TMA-gathered rows.  Measured (bench stage
+  // times): c3 / c4 31.9 -> 28.0 us, c2 22.8 -> 23.8 us (the 16-byte V copies compete
+  // with the A operand's cp.async), hence G >= 2 only.
+  constexpr bool TPV = VB == 16 && G >= 2;
   constexpr int kVHead = VB == 16 ? kDH * 2 : kDH * VB / 8 + (kDH / 32) * 4;   // value bytes per head-token
   constexpr int kVRow = 2 * kVHead;                                           // bytes of a V tile row (2 heads)
   constexpr int kVRowH = 2 * 144;   // (quantised) 8-bit recent-window row of the 2 heads (DESIGN R15)
@@ -252,7 +293,7 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
   float2* sQ = reinterpret_cast<float2*>(sV + kVBytes);          // [NQH][64] (q_lo, q_hi) per pair
   float* sL = reinterpret_cast<float*>(sQ + NQH * 64);           // [2 halves][NQH][128] partial logits
   float* sP = sL + 2 * NQH * kRows;                              // [NQH][kPS] probabilities
-  float* sRed = sP + NQH * kPS;                                  // [2 kinds][2 halves][4][G]
+  float* sRed = sP + (NQH * kPS > 1024 ? NQH * kPS : 1024);       // [2 kinds][2 halves][4][G]
   float* sAl = sRed + 2 * 2 * 4 * G;                             // [NQH] online-softmax rescale of the tile
   int* sIdxV = reinterpret_cast<int*>(sAl + NQH);                // [128] global rows of the V tile
   uint64_t* bars = reinterpret_cast<uint64_t*>(sIdxV + kRows);
@@ -262,7 +303,9 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
   uint64_t* tempty = tfull + 2;          // [2]
   uint64_t* vfull = tempty + 2;
   uint64_t* vempty = vfull + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(vempty + 1);
+  uint64_t* pready = vempty + 1;          // (TPV) [2] P of the tile written (epilogue -> MMA warp)
+  uint64_t* pvfull = pready + 2;          // (TPV) [2] O_tile in TMEM (tcgen05.commit -> epilogue)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pvfull + 2);
   int* s_thp = reinterpret_cast<int*>(tmem_slot + 1);   // first tile token read from the 8-bit recent window
   uint8_t* sVh = sV + kRows * kVRow;                      // (quantised) 8-bit rows of the recent window
   static_assert(VB == 16 || kRows * kVRow + 32 * 1280 <= kVBytes, "recent-window staging exceeds the V tile");
@@ -278,9 +321,13 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 128 + 1); mbar_init(&empty[s], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8); }
-    mbar_init(vfull, 1);
+    mbar_init(vfull, TPV ? 256 : 1);   // TPV: the 256 epilogue threads' cp.async; else one expect_tx
     mbar_init(vempty, 1);
+    for (int i = 0; i < 2; ++i) { mbar_init(&pready[i], 1); mbar_init(&pvfull[i], 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if constexpr (TPV) {   // P^T operands [2 heads][2 token blocks][8 rows x 128 B]: rows >= G stay zero
+    for (int i = tid; i < 4096 / 16; i += kThreads) reinterpret_cast<uint4*>(sP)[i] = make_uint4(0, 0, 0, 0);
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -350,14 +397,47 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
     // ================= MMA issuer =================
     if (lane == 0) {
       int u = 0;
+      int pv = 0;   // (TPV) next tile whose P V is to be issued
+      // P V of tile pv: 2 KV heads x 8 k-steps of 16 tokens into columns buf * 256 + kh * 8
+      // one tile per call; returns whether it issued (block: wait for the tile's P)
+      auto issue_pv = [&](bool block) -> bool {
+        if constexpr (TPV) {
+          if (pv < ntile) {
+            const int pb = pv & 1;
+            if (!block && !mbar_test(&pready[pb], (pv >> 1) & 1)) return false;
+            mbar_wait(&pready[pb], (pv >> 1) & 1);
+            tc_fence_after();
+            fence_proxy_async();
+#pragma unroll
+            for (int kh = 0; kh < 2; ++kh) {
+              const uint32_t va = smem_u32(sV + 2 * kh * (kRows * 128));
+              const uint32_t pa = smem_u32(sP) + kh * 2048;
+#pragma unroll
+              for (int kt = 0; kt < kRows / 16; ++kt)
+                mma_bf16_pv(tmem + pb * kBN + kh * 8, sw128_mn_desc(va + kt * 2048),
+                            sw128_desc(pa + (kt >> 2) * 1024 + (kt & 3) * 32), kt ? 1u : 0u);
+            }
+            mma_commit(&pvfull[pb]);
+            ++pv;
+            return true;
+          }
+        }
+        return false;
+      };
       for (int it = 0; it < ntile; ++it) {
         const int buf = it & 1;
-        if (it >= 2) mbar_wait(&tempty[buf], ((it >> 1) - 1) & 1);
+        if (it >= 2) {
+          if constexpr (TPV) { while (pv <= it - 2) issue_pv(true); }   // the epilogue frees buf only after P V
+          mbar_wait(&tempty[buf], ((it >> 1) - 1) & 1);
+        }
         TSTAMP(0 + it);
         tc_fence_after();
         const uint32_t acc = tmem + buf * kBN;
         for (int kc = 0; kc < nk; ++kc, ++u) {
           const int s = u % kStages;
+          if constexpr (TPV) {
+            while (!mbar_test(&full[s], (u / kStages) & 1)) issue_pv(false);
+          }
           mbar_wait(&full[s], (u / kStages) & 1);
           tc_fence_after();
           fence_proxy_async();
@@ -369,11 +449,15 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
         }
         mma_commit(&tfull[buf]);
         TSTAMP(8 + it);
+        while (issue_pv(false)) {}
       }
+      if constexpr (TPV) { while (pv < ntile) issue_pv(true); }
       // all MMAs issued: the next kernel may launch and run its pre-wait prologue
       // (the projection stages U, a weight) while this CTA's last epilogue runs
       pdl_launch_dependents();
     }
+  } else if (TPV && (warp == 2 || warp == 3)) {
+    // (TPV: the epilogue warps stage the V tiles themselves)
   } else if (warp == 2) {
     // ======== V rows producer: 32 TMA tile::gather4 of 4 x 512-B rows per tile; also
     // warms L2 with the next tile's V and latent rows ========
@@ -383,12 +467,15 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
     for (int it = 0; it < ntile; ++it) {
       const int tile = t_begin + it;
       const int nv = min(kRows, cnt - tile * kRows);
-      if (it >= 1) mbar_wait(vempty, (it - 1) & 1);     // previous tile's P V done with sV (and sIdxV)
+      int gi[4];   // the tile's gather rows, loaded BEFORE waiting for sV (the L2 round trip overlaps the P V)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int t = lane + 32 * j;
-        idx[t] = t < nv ? b * (int)a.cap + selb[tile * kRows + t] : -1;
+        gi[j] = t < nv ? b * (int)a.cap + selb[tile * kRows + t] : -1;
       }
+      if (it >= 1) mbar_wait(vempty, (it - 1) & 1);     // previous tile's P V done with sV (and sIdxV)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) idx[lane + 32 * j] = gi[j];
       __syncwarp();
       // quantised values with a recent window: tokens at positions >= s_b - w (a suffix of
       // the ascending tile) are read from the 8-bit ring (slot pos % w) into sVh
@@ -410,8 +497,8 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
         mbar_arrive_expect_tx(vfull, (uint32_t)(kRows * kVRow + n_hp * 4 * kVRowH));
       }
       __syncwarp();
-      tma_gather4(smem_u32(sV + lane * 4 * kVRow), &tmap_v, VB == 16 ? n0 : nb * kVRow, idx[4 * lane], idx[4 * lane + 1],
-                  idx[4 * lane + 2], idx[4 * lane + 3], vfull);
+      tma_gather4(smem_u32(sV + lane * 4 * kVRow), &tmap_v, VB == 16 ? n0 : nb * kVRow, idx[4 * lane],
+                  idx[4 * lane + 1], idx[4 * lane + 2], idx[4 * lane + 3], vfull);
       if (hp_lane) {
         int ri[4];
 #pragma unroll
@@ -485,6 +572,9 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
     // dims [8 (lane & 15), +8) of KV head kh = lane >> 4 (one 16-B V vector per token)
     const int kh = lane >> 4;
     float m_run[G], l_run[G], lp[G];   // lp: this warp's share of the softmax denominator of head kh*G+g
+    float ot[G], lt[G];                 // (TPV) o (dim n of KV head hf) and softmax denominator per query head
+#pragma unroll
+    for (int g = 0; g < G; ++g) { ot[g] = 0.f; lt[g] = 0.f; }
     float2 ov[G][4];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
@@ -493,11 +583,35 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
       for (int e = 0; e < 4; ++e) ov[g][e] = make_float2(0.f, 0.f);
     }
     const uint32_t tl = tmem + ((uint32_t)(rq * 32) << 16);
+    // the token row of tile it+1 is loaded during tile it (its L2 round trip would
+    // otherwise sit in front of the first RoPE angle of every tile)
+    int row_nx = m < min(kRows, cnt - t_begin * kRows) ? selb[t_begin * kRows + m] : -1;
     for (int it = 0; it < ntile; ++it) {
       const int tile = t_begin + it, buf = it & 1;
       const int nv = min(kRows, cnt - tile * kRows);
-      const int row = m < nv ? selb[tile * kRows + m] : -1;
+      const int row = row_nx;
+      if (it + 1 < ntile) row_nx = m < min(kRows, cnt - (tile + 1) * kRows) ? selb[(tile + 1) * kRows + m] : -1;
       const int pos = (int)a.pos_base + (row >= 0 ? row : 0);
+      if constexpr (TPV) {
+        // ---- stage the tile's V rows (the previous tile's P V has completed): this warp's 32
+        // tokens x the 256 bytes of KV head hf, 16-byte cp.async into the SWIZZLE_128B
+        // MN-major operand layout [64-dim block][token][128 B] (chunk c of token t at c ^ (t % 8));
+        // two tokens (256 contiguous bytes each) per instruction, in flight during the logits
+        const int cj = lane & 15;
+        const int dim = hf * kDH + 8 * cj;
+        const uint32_t vdst = smem_u32(sV) + (dim >> 6) * (kRows * 128);
+        const int ch = (dim & 63) >> 3;
+        const char* vsrc = reinterpret_cast<const char*>(a.v_cache) + ((size_t)n0 + dim) * 2;
+#pragma unroll 4
+        for (int q = 0; q < 16; ++q) {
+          const int tl = 2 * q + (lane >> 4);
+          const int t = rq * 32 + tl;
+          const int r = __shfl_sync(0xffffffffu, row, tl);
+          cp_async_16(vdst + t * 128 + ((ch ^ (t & 7)) << 4), vsrc + ((size_t)b * a.cap + (r >= 0 ? r : 0)) * a.D * 2,
+                      r >= 0 ? 16u : 0u);
+        }
+        cp_async_arrive_noinc(vfull);
+      }
       mbar_wait(&tfull[buf], (it >> 1) & 1);
       if (ew == 0 && lane == 0) TSTAMP(16 + it);
       tc_fence_after();
@@ -510,7 +624,7 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
       const float4* sQ4 = reinterpret_cast<const float4*>(sQ);
       // pairs per TMEM chunk: 8 for G = 4 (register pressure), else 16
       constexpr int PW = G >= 4 ? 8 : 16;
-#pragma unroll 1
+#pragma unroll   // (fully unrolled: the next chunk's angles are scheduled across the TMEM waits)
       for (int pc = 0; pc < 32 / PW; ++pc) {
         const int p0 = 32 * hf + PW * pc;
         float xl[2][PW], xh[2][PW];
@@ -561,9 +675,11 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
           }
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);     // this warp is done with the accumulator
+      if constexpr (!TPV) {   // (TPV: the buffer also receives the tile's P V; released after it)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);     // this warp is done with the accumulator
+      }
 #pragma unroll
       for (int j = 0; j < 2; ++j)
 #pragma unroll
@@ -589,7 +705,20 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
         mnew[g] = fmaxf(m_run[g], mt);
         alpha[g] = exp2f(m_run[g] - mnew[g]);        // m_run = -inf -> 0
         const float p = (row >= 0) ? exp2f(lg[g] - mnew[g]) : 0.f;
-        sP[(hf * G + g) * kPS + m] = p;
+        if constexpr (TPV) {
+          // bf16 P^T operand of KV head hf: [2 token blocks of 64][8 rows = query heads][128 B],
+          // SWIZZLE_128B (16-byte chunk (m % 64) / 8 of row g at chunk ^ g); the denominator
+          // sums the same rounded p the P V uses
+          const __nv_bfloat16 pb = __float2bfloat16_rn(p);
+          reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<uint8_t*>(sP) + hf * 2048 + (m >> 6) * 1024 + g * 128 +
+                                           ((((m & 63) >> 3) ^ g) << 4))[m & 7] = pb;
+          float ps = __bfloat162float(pb);
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
+          if (lane == 0) sRed[2 * 4 * G + (hf * 4 + rq) * G + g] = ps;
+        } else {
+          sP[(hf * G + g) * kPS + m] = p;
+        }
         m_run[g] = mnew[g];
         if (rq == 0 && lane == 0) sAl[hf * G + g] = alpha[g];
       }
@@ -597,6 +726,33 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
       bar_epi();                                       // sP / sAl of both halves visible
       mbar_wait(vfull, it & 1);
       if (ew == 0 && lane == 0) TSTAMP(32 + it);
+      if constexpr (TPV) {
+        // ---- P V on tcgen05: P^T (smem) and the V tile are complete -> the MMA warp issues the
+        // tile's 2 x 8 MMAs between its reconstruction chunks; O_tile^T (lane = dim n of KV head
+        // hf, column = query head) lands in columns buf * 256 + hf * 8 of the drained buffer
+        fence_proxy_async();   // this thread's P writes -> the tensor core's (async) proxy
+        bar_epi();
+        if (ew == 0 && lane == 0) mbar_arrive(&pready[buf]);
+        float tsum[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const float* r = sRed + 2 * 4 * G + hf * 4 * G + g;
+          tsum[g] = (r[0] + r[G]) + (r[2 * G] + r[3 * G]);
+          const float al = sAl[hf * G + g];
+          lt[g] = lt[g] * al + tsum[g];
+          ot[g] *= al;
+        }
+        mbar_wait(&pvfull[buf], (it >> 1) & 1);
+        tc_fence_after();
+        float od[8];
+        tmem_ld8_nowait(tl + buf * kBN + hf * 8, od);
+        tmem_wait_ld();
+#pragma unroll
+        for (int g = 0; g < G; ++g) ot[g] += od[g];
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);     // accumulator buffer (and its P V columns) free
+      } else
       // ---- P V: 16 tokens of this warp x 8 dims of KV head kh per lane, one 16-B V vector per token
       {
         float al[G];
@@ -682,6 +838,11 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
       if (ew == 0 && lane == 0) TSTAMP(40 + it);
       if (ew == 0 && lane == 0) mbar_arrive(vempty);
     }
+    float o[G];
+    if constexpr (TPV) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) { o[g] = ot[g]; l_run[g] = lt[g]; }
+    } else {
     // ---- reduce the 8 token groups' partial P V (sV is free: the V producer is done)
     float* red = reinterpret_cast<float*>(sV);   // [8 warps][NQH][128]
 #pragma unroll
@@ -701,13 +862,13 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
       for (int w = 0; w < 8; ++w) l += lred[w * NQH + hf * G + g];
       l_run[g] = l;
     }
-    float o[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       float acc = 0.f;
 #pragma unroll
       for (int w = 0; w < 8; ++w) acc += red[((size_t)w * NQH + hf * G + g) * kDH + n];
       o[g] = acc;
+    }
     }
     // ---- write y (single chunk) or the chunk's partial
 #pragma unroll
