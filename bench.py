@@ -62,6 +62,8 @@ def parse():
                     help="quantised value cache (SURVEY §8(f) f1): 4 or 2 bits, groups of 32 channels")
     ap.add_argument("--comm", choices=["lib", "torch"], default="lib",
                     help="c4-sharded exchange: the library's sals_decode_sharded or torch.distributed")
+    ap.add_argument("--batch", type=int, default=0, help="override the workload's batch (development)")
+    ap.add_argument("--seq", type=int, default=0, help="override the workload's sequence length, k = n/8 (development)")
     ap.add_argument("--separate-append", action="store_true",
                     help="sals_append_latent + sals_decode per layer instead of the fused sals_append_decode")
     return ap.parse_args()
@@ -76,6 +78,9 @@ def load_peaks():
     return PEAKS_FALLBACK, "fallback"
 
 
+SHAPE_OVERRIDE = {}   # --batch / --seq (development: e.g. the c5 sweep's B = 1 point with stage times)
+
+
 def workload_shape(name):
     if name == "all":   # the headline line's workload
         name = "c2"
@@ -83,6 +88,10 @@ def workload_shape(name):
     sh = dict(synth.CONFIGS[base])
     if base == "c5":   # single-point uses (the reference arm): the sweep's B = 8, n = 4K point
         sh.update(batch=8, seq=4096, top_k=512)
+    if SHAPE_OVERRIDE.get("batch"):
+        sh["batch"] = SHAPE_OVERRIDE["batch"]
+    if SHAPE_OVERRIDE.get("seq"):   # k = n / 8 as in every config
+        sh.update(seq=SHAPE_OVERRIDE["seq"], top_k=SHAPE_OVERRIDE["seq"] // 8)
     return base, sh
 
 
@@ -398,6 +407,9 @@ def measure(args, workload, rank, world, with_e2e=True):
         peaks, _ = load_peaks()
         dense = {"ms_per_step": dms, "tokens_per_s": world * B / (dms / 1e3),
                  "hbm_frac_of_measured": (dbytes * L / (dms / 1e3)) / (peaks["hbm_gbs"] * 1e9),
+                 # a dense decode AT the measured HBM peak (its K / V bytes only): the
+                 # comparator-independent bound SALS is also reported against
+                 "roofline_ms_per_step": dbytes * L / (peaks["hbm_gbs"] * 1e9) * 1e3,
                  "kernel": "in-build split-K flash decode over the full post-RoPE K/V cache"}
         del gd, wsd
 
@@ -427,6 +439,7 @@ def measure(args, workload, rank, world, with_e2e=True):
         "e2e": e2e,
         "dense": dense,
         "speedup_vs_dense": (dense["ms_per_step"] / ms) if dense else None,
+        "speedup_vs_dense_roofline": (dense["roofline_ms_per_step"] / ms) if dense else None,
         "sh": sh,
     }
     del layers, g, ws, out
@@ -445,6 +458,7 @@ def summary_of(w, r):
         "tokens_per_s": round(r["value"], 1),
         "e2e_tokens_per_s": round(r["e2e"]["value"], 1) if r["e2e"] else None,
         "vs_dense": round(r["speedup_vs_dense"], 3) if r["speedup_vs_dense"] else None,
+        "vs_dense_at_hbm_roofline": round(r["speedup_vs_dense_roofline"], 3) if r["speedup_vs_dense_roofline"] else None,
         "dense_us_per_layer_step": round(r["dense"]["ms_per_step"] * 1e3 / r["config"]["layers"], 2) if r["dense"] else None,
         "dense_hbm_frac_of_measured": round(r["dense"]["hbm_frac_of_measured"], 3) if r["dense"] else None,
         "stages_us": r["stages_us"],
@@ -476,6 +490,7 @@ def run_sals(args, rank, world):
     if r["dense"]:
         line["dense"] = r["dense"]
         line["speedup_vs_dense"] = r["speedup_vs_dense"]
+        line["speedup_vs_dense_roofline"] = r["speedup_vs_dense_roofline"]
     if len(names) > 1:
         line["workloads"] = {w: summary_of(w, res[w]) for w in names}
         line["gpu_launches_all_workloads"] = sum(res[w]["gpu_launches"] for w in names)
@@ -719,6 +734,7 @@ def roofline(sh, stages, peaks, peak_kind, v_row_bytes=None):
 
 def main():
     args = parse()
+    SHAPE_OVERRIDE.update(batch=args.batch, seq=args.seq)
     rank, world, local = dist_init(args.gpus)
     try:
         if args.impl == "reference":

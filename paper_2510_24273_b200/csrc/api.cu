@@ -230,7 +230,7 @@ int flash_tpw_unr(const sals_config* c) {
   const int epl = c->dtype == SALS_BF16 ? 8 : 4;
   const int lpt = c->head_dim / epl;
   const int G = c->num_q_heads / c->num_kv_heads;
-  return (32 / lpt) * (G <= 4 ? 4 : 2);   // flash_decode_kernel TPW * UNR
+  return (32 / lpt) * (G <= 2 ? 4 : 2);   // flash_decode_kernel TPW * UNR
 }
 
 // Rows of U per CTA of the projection cluster: a multiple of 8 (16-byte vectors),
@@ -420,8 +420,11 @@ sals_status launch_flash(const sals_config* c, FlashArgs a, int batch, cudaStrea
   }
 #undef SALS_FD_CASE
   if (!k) return fail(SALS_ERR_UNSUPPORTED, "flash decode shape");
-  dim3 grid(ceil_div(a.nsplit, 4), c->num_kv_heads, batch);
-  SALS_CUDA_TRY(launch(k, grid, dim3(128), 0, st, 0, a));
+  // one CTA = one split x up to 8 consecutive KV heads (their row segments are contiguous)
+  int hpc = 8;
+  while (c->num_kv_heads % hpc) hpc >>= 1;
+  dim3 grid(a.nsplit, c->num_kv_heads / hpc, batch);
+  SALS_CUDA_TRY(launch(k, grid, dim3(32 * hpc), 0, st, 0, a));
   return SALS_OK;
 }
 
