@@ -236,26 +236,40 @@ sals_status sals_dense_decode(const sals_config* cfg, const void* q, const void*
 /*
  * Sequence-sharded decode — the three device phases around the
  * two exchanges.  Rank p holds the contiguous positions
- * [shard_start, shard_start + local_len_b) of every request b.  The caller
- * (one process per GPU) all-gathers between the phases over NCCL:
+ * [shard_start, shard_start + local_len_b) of every request b; ranks are in
+ * ascending position order.  The caller (one process per GPU) all-gathers
+ * between the phases over NCCL:
  *  1. sals_shard_candidates: local q~, p' over the shard, and the local top
  *     min(k-x-z, n_ranked) of the ranked range [x, s_b-z) with GLOBAL indices,
  *     ascending index order, padded with (idx -1, score -inf) to k entries.
  *       cand_score [B, k] fp32, cand_idx [B, k] int32 (outputs)
- *  2. (caller) all-gather -> cand_all_* [P, B, k] in rank order.
  *     It also leaves the rotated query q^R in `workspace`, which phase 3 reads:
  *     sals_shard_attend must be given the SAME workspace, unmodified in between
  *     (sals_decode_sharded does this itself).
- *  3. sals_shard_attend: global TopK over the P*k candidates with the same
- *     policy and tie-break as sals_decode (identical on every rank), then
- *     reconstruct + RoPE + attention over the OWNED selected tokens (plus the
- *     owned sink / recent ones) -> partial (m, l, o) per (b, query head):
+ *  2. (caller) all-gather of the SCORES only -> cand_all_score [P, B, k] in rank
+ *     order.  The indices stay local: since the shards are contiguous and every
+ *     list is ascending, the gathered order (rank, position) IS the global index
+ *     order, which is all the tie-break (lower index first, R5) needs.
+ *  3. sals_shard_attend(..., cand_all_score, cand_idx = this rank's phase-1
+ *     indices, world, rank, ...): the exact global TopK of Alg. 1 line 5
+ *     over the union -- the (k-x-z)-th largest score T by a radix select over
+ *     the P*k gathered scores and the quota of ties at T, ranks in order -- fused
+ *     with this rank's owned list (owned sinks | its candidates above T and its
+ *     share of the ties | owned recents), then reconstruct + RoPE + attention
+ *     over the owned tokens -> partial (m, l, o) per (b, query head):
  *       partial [B, n_q, d+2] fp32: m (log2 domain), l, o[d]
  *  4. (caller) all-gather -> partial_all [P, B, n_q, d+2].
  *  5. sals_merge_partials: log-sum-exp merge -> out [B, n_q*d] (every rank).
  * With P = 1 the result equals sals_decode's (bit-identical selection).
  *   d_local_len [B] int32 device, d_seq_len [B] int32 device (global s_b).
  */
+/* Inspection: byte offsets, inside a workspace of sals_workspace_bytes /
+ * sals_shard_workspace_bytes(cfg, batch, max_seq_len (max_local_len), ...), of the
+ * selection list [B, k] int32 (sals_decode: selected positions, ascending, -1
+ * padded; sals_shard_attend: the owned LOCAL rows, ascending) and its counts [B]
+ * int32, valid after the call that wrote them completes. */
+sals_status sals_workspace_selection_offsets(const sals_config* cfg, int32_t batch, int32_t max_seq_len,
+                                             size_t* off_sel, size_t* off_count);
 sals_status sals_shard_candidates(const sals_config* cfg, const void* U, const void* q,
                                   const void* latent_shard, int64_t cap_local, int32_t batch,
                                   int64_t shard_start, const int32_t* d_local_len,
@@ -266,9 +280,9 @@ sals_status sals_shard_attend(const sals_config* cfg, const void* U, const void*
                               const void* latent_shard, const void* v_shard, int64_t cap_local,
                               int32_t batch, int64_t shard_start, const int32_t* d_local_len,
                               int32_t max_local_len, const int32_t* d_seq_len,
-                              const float* cand_all_score, const int32_t* cand_all_idx,
-                              int32_t world, float* partial, void* workspace, size_t ws_bytes,
-                              void* stream);
+                              const float* cand_all_score, const int32_t* cand_idx,
+                              int32_t world, int32_t rank, float* partial, void* workspace,
+                              size_t ws_bytes, void* stream);
 sals_status sals_merge_partials(const sals_config* cfg, const float* partial_all, int32_t world,
                                 int32_t batch, void* out, void* stream);
 size_t sals_shard_workspace_bytes(const sals_config* cfg, int32_t batch, int32_t max_local_len,
@@ -289,7 +303,8 @@ size_t sals_shard_workspace_bytes(const sals_config* cfg, int32_t batch, int32_t
  *    holds global positions [shard_start, shard_start + local_len_b) of every
  *    request); workspace of sals_decode_sharded_workspace_bytes(cfg, B,
  *    max_local_len, world) bytes holds the phases' workspace plus the gathered
- *    candidates [P, B, k] x (fp32, int32) and partials [P, B, n_q, d+2] fp32.
+ *    candidate scores [P, B, k] fp32, this rank's candidate indices [B, k] int32
+ *    and the gathered partials [P, B, n_q, d+2] fp32.
  *    With world = 1 the result equals sals_decode's.  The quantised values'
  *    recent window is not sharded (SALS_ERR_UNSUPPORTED).
  */

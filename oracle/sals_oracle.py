@@ -295,6 +295,34 @@ def global_select(cand_scores: np.ndarray, cand_idx: np.ndarray, s: int, cfg: Co
     return np.sort(np.concatenate([forced, ci[order]]))
 
 
+def shard_owned_selection(gathered_scores: np.ndarray, own_idx: np.ndarray, rank: int, lo: int, hi: int, s: int,
+                          cfg: Config) -> np.ndarray:
+    """One rank's part of the global selection when only the candidate SCORES are exchanged (§8(e)).
+
+    gathered_scores [P, kc]: every rank's ranked candidates (ascending global index, -inf padded),
+    in rank order; own_idx [kc]: this rank's global indices (-1 padded); this rank holds [lo, hi).
+    The shards are contiguous and ascending, so the gathered order (rank, position) is the global
+    index order: the global TopK of the union by (score desc, index asc) -- ``select_topk``'s rule
+    -- is fixed without the other ranks' indices.  Returns this rank's selected positions plus its
+    forced sink / recent ones, ascending (global indices)."""
+    hi = min(hi, s)
+    if s <= cfg.top_k:
+        return np.arange(lo, max(lo, hi), dtype=np.int64)
+    x, z = cfg.sink, cfg.recent
+    y = cfg.top_k - x - z
+    P, kc = gathered_scores.shape
+    rk, pos = np.meshgrid(np.arange(P), np.arange(kc), indexing="ij")
+    sc, rk, pos = gathered_scores.ravel(), rk.ravel(), pos.ravel()
+    valid = ~np.isneginf(sc)
+    sc, rk, pos = sc[valid], rk[valid], pos[valid]
+    order = np.lexsort((pos, rk, -sc))[:y]
+    mine = pos[order][rk[order] == rank]
+    picks = own_idx[mine].astype(np.int64)
+    forced = np.concatenate([np.arange(0, x), np.arange(s - z, s)]).astype(np.int64)
+    forced = forced[(forced >= lo) & (forced < hi)]
+    return np.sort(np.concatenate([forced, picks]))
+
+
 def partial_attention(qR: np.ndarray, KR: np.ndarray, V: np.ndarray, cfg: Config):
     """Per query head (m, l, o) over a token subset: m = max logit, l = sum e^{l-m}, o = sum e^{l-m} v."""
     nq, d = cfg.num_q_heads, cfg.head_dim

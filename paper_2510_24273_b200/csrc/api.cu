@@ -26,6 +26,8 @@ std::atomic<uint64_t> g_launches{0};
 
 // Optional per-stage event recorder (sals_decode_profile only).
 enum { kStQproj = 0, kStScore, kStTopk, kStReconAttn, kStFlash, kStMerge, kNumStages };
+constexpr int kStExchange = kNumStages + 1;   // (sharded) the NCCL all-gathers; bit kNumStages is the append
+constexpr int kStShardSelect = kNumStages + 2; // (sharded) global selection + owned list
 struct StageTimer {
   cudaEvent_t ev[kNumStages + 1];
   float ms[kNumStages];
@@ -170,7 +172,7 @@ struct Plan {
   size_t tk_smem;
   int proj_cs, proj_rows;
   // workspace offsets
-  size_t off_qtil, off_qrope, off_scores, off_sel, off_count, off_kr, off_part, off_hist, total;
+  size_t off_qtil, off_qrope, off_scores, off_sel, off_count, off_ccount, off_kr, off_part, off_hist, total;
   int hist_words;          // histogram + (tcgen05 v2) split-merge counters, zeroed by the query projection
   int64_t score_stride;
 };
@@ -181,38 +183,30 @@ bool tc_eligible(const sals_config* c, int batch, int kmax) {
          c->num_q_heads / c->num_kv_heads);
 }
 
-// Top-k cluster plan.  cand == true: the generic kernel over all-gathered
-// candidates (K9); else the histogram-assisted kernel (K4 / K8).
+// Top-k cluster plan of the histogram-assisted kernel (K4 / K8).
 constexpr size_t kTopkDynSmem = 190 * 1024;
 // 16-CTA cluster x 23808-entry slices: slice * 8 B + 1024 candidates x 4 B = 190 KB (plan_topk)
 constexpr int kMaxSeqLen = 16 * 23808;
-sals_status plan_topk(int n_entries, bool cand, Plan& p) {
+sals_status plan_topk(int n_entries, Plan& p) {
   static const int slice_env = [] { const char* e = getenv("SALS_TOPK_SLICE"); return e ? atoi(e) : 0; }();
   const int target = (slice_env >= 256 && slice_env <= 16384) ? slice_env : 2048;   // experiment override
   int cs = 1;
   while (cs < 16 && ceil_div(n_entries, cs) > target) cs <<= 1;
   int slice = ceil_div(n_entries, cs);
   slice = (int)align_up(std::max(slice, 4), 4);
-  const int cap = cand ? 16384 : 24576;
-  if (slice > cap) return fail(SALS_ERR_UNSUPPORTED, "top-k over %d entries exceeds the cluster limit", n_entries);
+  if (slice > 24576) return fail(SALS_ERR_UNSUPPORTED, "top-k over %d entries exceeds the cluster limit", n_entries);
   p.tk_cs = cs;
   p.tk_slice = slice;
   p.tk_n = n_entries;
-  if (cand) {
-    p.tk_nt = kTopkThreads;
-    p.tk_cap = 0;
-    p.tk_smem = ((size_t)slice * 9 + 15) / 16 * 16 + (size_t)(kTopkThreads / 32) * 256 * 4;
-  } else {
-    p.tk_nt = slice >= 4096 ? 1024 : 512;
-    // signed: the staged slice (8 B per entry) plus a candidate area of at least
-    // kMinCand entries must fit the kernel's dynamic shared memory
-    constexpr int64_t kMinCand = 1024;
-    const int64_t avail = (int64_t)kTopkDynSmem - (int64_t)slice * 8;
-    if (avail < kMinCand * 4)
-      return fail(SALS_ERR_UNSUPPORTED, "top-k over %d entries exceeds the cluster's shared memory", n_entries);
-    p.tk_cap = (int)std::min<int64_t>(kCandCap, avail / 4);
-    p.tk_smem = (size_t)slice * 8 + (size_t)p.tk_cap * 4;
-  }
+  p.tk_nt = slice >= 4096 ? 1024 : 512;
+  // signed: the staged slice (8 B per entry) plus a candidate area of at least
+  // kMinCand entries must fit the kernel's dynamic shared memory
+  constexpr int64_t kMinCand = 1024;
+  const int64_t avail = (int64_t)kTopkDynSmem - (int64_t)slice * 8;
+  if (avail < kMinCand * 4)
+    return fail(SALS_ERR_UNSUPPORTED, "top-k over %d entries exceeds the cluster's shared memory", n_entries);
+  p.tk_cap = (int)std::min<int64_t>(kCandCap, avail / 4);
+  p.tk_smem = (size_t)slice * 8 + (size_t)p.tk_cap * 4;
   return SALS_OK;
 }
 
@@ -270,7 +264,7 @@ sals_status make_plan(const sals_config* c, int batch, int max_s, Plan& p, bool 
   } else {
     plan_flash(batch, c->num_kv_heads, p.kmax, flash_tpw_unr(c), p.nsplit, p.chunk);
   }
-  sals_status st = plan_topk(max_s, false, p);
+  sals_status st = plan_topk(max_s, p);
   if (st != SALS_OK) return st;
   plan_proj(p, true);
   const size_t es = esize(c);
@@ -282,6 +276,7 @@ sals_status make_plan(const sals_config* c, int batch, int max_s, Plan& p, bool 
   p.off_scores = take((size_t)batch * p.score_stride * 4);
   p.off_sel = take((size_t)batch * c->top_k * 4);
   p.off_count = take((size_t)batch * 4);
+  p.off_ccount = take((size_t)batch * 4);   // (sharded) valid local candidates per request
   p.off_kr = take(p.tc ? 0 : (size_t)batch * c->top_k * p.D * es);
   p.off_part = take((size_t)batch * c->num_q_heads * p.nsplit * (c->head_dim + 2) * 4);
   p.hist_words = batch * kH0Bins + (p.tc2 ? batch * (p.D / 256) : 0);
@@ -362,18 +357,14 @@ sals_status launch_topk(TopkArgs a, int batch, const Plan& p, cudaStream_t st) {
   SALS_CUDA_TRY(once.run([] {
     auto* k512 = topk_hist_kernel<512>;
     auto* k1024 = topk_hist_kernel<1024>;
-    cudaError_t e = cudaFuncSetAttribute(topk_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTopkDynSmem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(topk_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k512, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTopkDynSmem);
+    cudaError_t e = cudaFuncSetAttribute(k512, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTopkDynSmem);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k512, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k1024, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTopkDynSmem);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k1024, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     return e;
   }));
   // cluster attribute even for cs == 1 (the kernels use cluster barriers / DSMEM)
-  if (a.hist0 == nullptr) {
-    SALS_CUDA_TRY(launch(topk_cluster_kernel, dim3(batch * p.tk_cs), dim3(kTopkThreads), p.tk_smem, st, p.tk_cs, a));
-  } else if (a.cand_idx == nullptr && a.seg_len == 0 && p.tk_n <= 8192 && !g_topk_cluster) {
+  if (p.tk_n <= 8192 && !g_topk_cluster) {
     cudaError_t e = launch_topk_cta(a, batch, p.tk_n, st);
     if (e != cudaSuccess) return fail(SALS_ERR_CUDA, "topk_cta launch: %s", cudaGetErrorString(e));
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -594,6 +585,19 @@ uint32_t sals_profile_stage_mask(uint32_t mask) {
 
 uint64_t sals_launch_count(int32_t reset) {
   return reset ? g_launches.exchange(0) : g_launches.load();
+}
+
+sals_status sals_workspace_selection_offsets(const sals_config* cfg, int32_t batch, int32_t max_seq_len,
+                                             size_t* off_sel, size_t* off_count) {
+  sals_status s = validate(cfg);
+  if (s != SALS_OK) return s;
+  if (!off_sel || !off_count || batch < 1 || max_seq_len < 1) return fail(SALS_ERR_INVALID_ARGUMENT, "bad arguments");
+  Plan p{};
+  s = make_plan(cfg, batch, max_seq_len, p, true);
+  if (s != SALS_OK) return s;
+  *off_sel = p.off_sel;
+  *off_count = p.off_count;
+  return SALS_OK;
 }
 
 size_t sals_workspace_bytes(const sals_config* cfg, int32_t batch, int32_t max_seq_len) {
@@ -820,8 +824,7 @@ size_t sals_shard_workspace_bytes(const sals_config* cfg, int32_t batch, int32_t
   if (validate(cfg) != SALS_OK || batch < 1 || max_local_len < 1 || world < 1) return 0;
   Plan p{};
   if (make_plan(cfg, batch, std::max(max_local_len, 1), p, true) != SALS_OK) return 0;
-  // extra: global selection [B, k] + count
-  return align_up(p.total, 256) + align_up((size_t)batch * cfg->top_k * 4, 256) + align_up((size_t)batch * 4, 256);
+  return align_up(p.total, 256);
 }
 
 sals_status sals_shard_candidates(const sals_config* cfg, const void* U, const void* q, const void* latent_shard,
@@ -856,11 +859,11 @@ sals_status sals_shard_candidates(const sals_config* cfg, const void* U, const v
   sa.len = d_local_len; sa.scores = scores; sa.stride = p.score_stride;
   sa.hist0 = hist; sa.seq_len = d_seq_len; sa.idx_base = shard_start; sa.sink = cfg->sink; sa.recent = cfg->recent;
   if (cfg->dtype == SALS_BF16) {
-    s = launch_project<__nv_bfloat16>(cfg, p, 1, pa, st);
-    if (s == SALS_OK) s = launch_score<__nv_bfloat16>(cfg, sa, batch, max_local_len, st);
+    if (on(kStQproj)) s = launch_project<__nv_bfloat16>(cfg, p, 1, pa, st);
+    if (s == SALS_OK && on(kStScore)) s = launch_score<__nv_bfloat16>(cfg, sa, batch, max_local_len, st);
   } else {
-    s = launch_project<float>(cfg, p, 1, pa, st);
-    if (s == SALS_OK) s = launch_score<float>(cfg, sa, batch, max_local_len, st);
+    if (on(kStQproj)) s = launch_project<float>(cfg, p, 1, pa, st);
+    if (s == SALS_OK && on(kStScore)) s = launch_score<float>(cfg, sa, batch, max_local_len, st);
   }
   if (s != SALS_OK) return s;
   TopkArgs ta{};
@@ -868,21 +871,22 @@ sals_status sals_shard_candidates(const sals_config* cfg, const void* U, const v
   ta.idx_base = shard_start; ta.k = cfg->top_k; ta.sink = cfg->sink; ta.recent = cfg->recent; ta.mode = 1;
   ta.slice = p.tk_slice; ta.sel_out = cand_idx; ta.sel_stride = cfg->top_k; ta.sel_score = cand_score;
   ta.pad_to = cfg->top_k;
+  ta.sel_count = reinterpret_cast<int*>(ws + p.off_ccount);   // read by the selection (shard.cu)
   ta.hist0 = hist;
-  return launch_topk(ta, batch, p, st);
+  return on(kStTopk) ? launch_topk(ta, batch, p, st) : SALS_OK;
 }
 
 sals_status sals_shard_attend(const sals_config* cfg, const void* U, const void* q, const void* latent_shard,
                               const void* v_shard, int64_t cap_local, int32_t batch, int64_t shard_start,
                               const int32_t* d_local_len, int32_t max_local_len, const int32_t* d_seq_len,
-                              const float* cand_all_score, const int32_t* cand_all_idx, int32_t world,
+                              const float* cand_all_score, const int32_t* cand_idx, int32_t world, int32_t rank,
                               float* partial, void* workspace, size_t ws_bytes, void* stream) {
   sals_status s = validate(cfg);
   if (s != SALS_OK) return s;
-  if (!U || !q || !latent_shard || !v_shard || !d_local_len || !d_seq_len || !cand_all_score || !cand_all_idx ||
+  if (!U || !q || !latent_shard || !v_shard || !d_local_len || !d_seq_len || !cand_all_score || !cand_idx ||
       !partial || !workspace)
     return fail(SALS_ERR_INVALID_ARGUMENT, "NULL tensor argument");
-  if (world < 1 || batch < 1 || max_local_len < 1 || max_local_len > cap_local)
+  if (world < 1 || rank < 0 || rank >= world || batch < 1 || max_local_len < 1 || max_local_len > cap_local)
     return fail(SALS_ERR_INVALID_ARGUMENT, "bad shard geometry");
   if (hp_window(cfg)) return fail(SALS_ERR_UNSUPPORTED, "the quantised values' recent window is not sharded");
   Plan p{};
@@ -890,28 +894,19 @@ sals_status sals_shard_attend(const sals_config* cfg, const void* U, const void*
   if (s != SALS_OK) return s;
   if (ws_bytes < sals_shard_workspace_bytes(cfg, batch, max_local_len, world))
     return fail(SALS_ERR_WORKSPACE_TOO_SMALL, "shard workspace too small");
-  // top-k over the gathered candidates: its own cluster plan
-  Plan pk{};
-  s = plan_topk(world * cfg->top_k, true, pk);
-  if (s != SALS_OK) return s;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   char* ws = reinterpret_cast<char*>(workspace);
-  int* gsel = reinterpret_cast<int*>(ws + align_up(p.total, 256));
-  int* gcount = reinterpret_cast<int*>(ws + align_up(p.total, 256) + align_up((size_t)batch * cfg->top_k * 4, 256));
   int* own = reinterpret_cast<int*>(ws + p.off_sel);
   int* own_count = reinterpret_cast<int*>(ws + p.off_count);
-  TopkArgs ta{};
-  ta.scores = cand_all_score; ta.cand_idx = cand_all_idx; ta.n_const = world * cfg->top_k;
-  ta.seg_len = cfg->top_k; ta.seg_stride = (int64_t)batch * cfg->top_k; ta.seq_len = d_seq_len;
-  ta.k = cfg->top_k; ta.sink = cfg->sink; ta.recent = cfg->recent; ta.mode = 1; ta.slice = pk.tk_slice;
-  ta.sel_out = gsel; ta.sel_stride = cfg->top_k; ta.sel_count = gcount; ta.pad_to = cfg->top_k;
-  s = launch_topk(ta, batch, pk, st);
-  if (s != SALS_OK) return s;
-  OwnedArgs oa{};
-  oa.gsel = gsel; oa.gcount = gcount; oa.g_stride = cfg->top_k; oa.seq_len = d_seq_len; oa.local_len = d_local_len;
-  oa.shard_start = shard_start; oa.sink = cfg->sink; oa.recent = cfg->recent; oa.k = cfg->top_k;
-  oa.own_sel = own; oa.own_count = own_count;
-  SALS_CUDA_TRY(launch(owned_list_kernel, dim3(batch), dim3(256), 0, st, 0, oa));
+  // global selection from the gathered scores fused with this rank's owned list (shard.cu)
+  ShardSelectArgs sa{};
+  sa.all_score = cand_all_score; sa.own_idx = cand_idx; sa.world = world; sa.rank = rank; sa.batch = batch;
+  sa.kc = cfg->top_k; sa.seq_len = d_seq_len; sa.local_len = d_local_len; sa.shard_start = shard_start;
+  sa.k = cfg->top_k; sa.sink = cfg->sink; sa.recent = cfg->recent; sa.own_sel = own; sa.own_count = own_count;
+  sa.cand_count = reinterpret_cast<const int*>(ws + p.off_ccount);
+  // one rank: the selection is every local candidate -- a parallel copy over kSelCopyCtas CTAs
+  if (on(kStShardSelect))
+    SALS_CUDA_TRY(launch(shard_select_kernel, dim3(batch, world == 1 ? kSelCopyCtas : 1), dim3(1024), 0, st, 0, sa));
   if (cfg->dtype == SALS_BF16)
     return attend_list<__nv_bfloat16>(cfg, p, U, latent_shard, v_shard, cap_local, batch, shard_start, own,
                                       own_count, ws, nullptr, partial, st);
@@ -987,9 +982,9 @@ ShardLayout shard_layout(const sals_config* cfg, int32_t batch, int32_t max_loca
   L.base = align_up(sals_shard_workspace_bytes(cfg, batch, max_local_len, world), 256);
   const size_t cand = align_up((size_t)world * batch * cfg->top_k * 4, 256);
   const size_t part = (size_t)batch * cfg->num_q_heads * (cfg->head_dim + 2) * 4;
-  L.cand_s = L.base;
-  L.cand_i = L.cand_s + cand;
-  L.part_all = L.cand_i + cand;
+  L.cand_s = L.base;                                                  // [P, B, k] gathered scores
+  L.cand_i = L.cand_s + cand;                                         // [B, k] this rank's indices
+  L.part_all = L.cand_i + align_up((size_t)batch * cfg->top_k * 4, 256);
   L.total = L.part_all + align_up(part * world, 256);
   return L;
 }
@@ -1057,22 +1052,20 @@ sals_status sals_decode_sharded(const sals_config* cfg, void* comm, const void* 
   int32_t* cand_i = reinterpret_cast<int32_t*>(ws + L.cand_i);
   float* part_all = reinterpret_cast<float*>(ws + L.part_all);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  // 1. local candidates straight into this rank's slot of the gather buffers
+  // 1. local candidates: scores straight into this rank's slot of the gather buffer,
+  //    global indices kept locally (the gathered order (rank, position) is the index order)
   s = sals_shard_candidates(cfg, U, q, latent_shard, cap_local, batch, shard_start, d_local_len, max_local_len,
-                            d_seq_len, cand_s + me * nc, cand_i + me * nc, workspace, L.base, stream);
+                            d_seq_len, cand_s + me * nc, cand_i, workspace, L.base, stream);
   if (s != SALS_OK) return s;
-  // 2. in-place all-gather of (score, index): one NCCL group, rank order
-  SALS_NCCL_TRY(nccl().group_start());
-  SALS_NCCL_TRY(nccl().all_gather(cand_s + me * nc, cand_s, nc, ncclFloat32, c->comm, st));
-  SALS_NCCL_TRY(nccl().all_gather(cand_i + me * nc, cand_i, nc, ncclInt32, c->comm, st));
-  SALS_NCCL_TRY(nccl().group_end());
-  // 3. global selection + attention over the owned tokens -> this rank's partial slot
+  // 2. in-place all-gather of the candidate scores (rank order)
+  if (on(kStExchange)) SALS_NCCL_TRY(nccl().all_gather(cand_s + me * nc, cand_s, nc, ncclFloat32, c->comm, st));
+  // 3. global selection + owned list (one kernel), attention over the owned tokens -> partial slot
   s = sals_shard_attend(cfg, U, q, latent_shard, v_shard, cap_local, batch, shard_start, d_local_len, max_local_len,
-                        d_seq_len, cand_s, cand_i, P, part_all + me * np, workspace, L.base, stream);
+                        d_seq_len, cand_s, cand_i, P, me, part_all + me * np, workspace, L.base, stream);
   if (s != SALS_OK) return s;
   // 4. in-place all-gather of the partials, 5. merge on every rank
-  SALS_NCCL_TRY(nccl().all_gather(part_all + me * np, part_all, np, ncclFloat32, c->comm, st));
-  return sals_merge_partials(cfg, part_all, P, batch, out, stream);
+  if (on(kStExchange)) SALS_NCCL_TRY(nccl().all_gather(part_all + me * np, part_all, np, ncclFloat32, c->comm, st));
+  return on(kStMerge) ? sals_merge_partials(cfg, part_all, P, batch, out, stream) : SALS_OK;
 }
 
 }  // extern "C"

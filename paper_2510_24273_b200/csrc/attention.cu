@@ -5,7 +5,6 @@
 //                           (Alg. 1 lines 8-9 / Eq. 6; also the dense flash decode)
 //   merge_kernel            log-sum-exp merge of the split partials -> y
 //   dense_append_kernel     post-RoPE dense cache write (comparator)
-//   owned_list_kernel       sharded: local rows a rank attends to
 #include "common.cuh"
 #include "kernels.h"
 
@@ -388,36 +387,4 @@ template __global__ void dense_append_kernel<__nv_bfloat16>(DenseAppendArgs);
 // ---------------------------------------------------------------------------
 // Sharded: the rows this rank attends to = owned sinks, owned global picks,
 // owned recents (three ascending, disjoint, ordered ranges).  One CTA / request.
-// ---------------------------------------------------------------------------
-__global__ void owned_list_kernel(OwnedArgs a) {
-  const int b = blockIdx.x;
-  __shared__ int s_cnt[3], s_first;
-  pdl_wait();
-  const int s = a.seq_len[b];
-  const int64_t lo = a.shard_start, hi = a.shard_start + a.local_len[b];
-  const int gcnt = a.gcount[b];
-  const int* gs = a.gsel + (size_t)b * a.g_stride;
-  int* own = a.own_sel + (size_t)b * a.k;
-  // forced ranges (s > k only; when s <= k the global picks are every ranked token and
-  // the forced ranges are still [0,x) and [s-z,s) clipped to [0,s))
-  const int x = min(a.sink, s), z0 = max(x, s - a.recent);
-  const int64_t sk0 = max(lo, (int64_t)0), sk1 = min(hi, (int64_t)x);
-  const int64_t rc0 = max(lo, (int64_t)z0), rc1 = min(hi, (int64_t)s);
-  const int nsk = (int)max((int64_t)0, sk1 - sk0), nrc = (int)max((int64_t)0, rc1 - rc0);
-  if (threadIdx.x == 0) { s_cnt[0] = 0; s_first = gcnt; }
-  __syncthreads();
-  // global picks are ascending: owned ones form one contiguous run
-  for (int i = threadIdx.x; i < gcnt; i += blockDim.x) {
-    const int gi = gs[i];
-    if (gi >= lo && gi < hi) { atomicAdd(&s_cnt[0], 1); atomicMin(&s_first, i); }
-  }
-  __syncthreads();
-  const int ng = s_cnt[0], f = s_first;
-  for (int i = threadIdx.x; i < nsk; i += blockDim.x) own[i] = (int)(sk0 + i - lo);
-  for (int i = threadIdx.x; i < ng; i += blockDim.x) own[nsk + i] = (int)(gs[f + i] - lo);
-  for (int i = threadIdx.x; i < nrc; i += blockDim.x) own[nsk + ng + i] = (int)(rc0 + i - lo);
-  if (threadIdx.x == 0) a.own_count[b] = nsk + ng + nrc;
-  pdl_launch_dependents();
-}
-
 }  // namespace sals

@@ -13,7 +13,6 @@ namespace sals {
 // Block sizes shared by kernels and launcher.
 constexpr int kProjThreads = 256;
 constexpr int kScoreThreads = 256;
-constexpr int kTopkThreads = 1024;
 // First radix digit of the top-k, built by the score kernel: the top 11 bits of
 // the order-preserving float key of every ranked score.
 constexpr int kH0Bits = 11, kH0Bins = 1 << kH0Bits, kH0Shift = 32 - kH0Bits;
@@ -60,11 +59,9 @@ struct ScoreArgs {
 
 struct TopkArgs {
   const float* scores; int64_t score_stride;  // [B, stride]
-  const int* cand_idx;    // nullable: global index of each entry (-1 = empty)
-  const int* n_entries;   // nullable: entries of request b (else n_const)
-  int n_const;
+  const int* n_entries;   // nullable: entries of request b (else seq_len[b])
   const int* seq_len;     // [B] global s_b
-  int64_t idx_base;       // global index of entry 0 when cand_idx == nullptr
+  int64_t idx_base;       // global index of entry 0 (shard start)
   int k, sink, recent;
   int mode;               // 0 = full Alg. 1 selection; 1 = ranked-range candidates only
   int slice;              // entries per CTA
@@ -73,8 +70,6 @@ struct TopkArgs {
   int* sel_count;         // nullable [B]
   int pad_to;             // -1 padding up to this many entries
   int* sel_out2;          // nullable second copy of sel_out (user buffer), stride sel_stride
-  int seg_len;            // >0: entries are [world][B][seg_len] (all-gathered candidates)
-  int64_t seg_stride;     //     = B * seg_len
   const uint32_t* hist0;  // nullable [B, kH0Bins] from the score kernel: histogram-assisted path
   int cand_cap;           // histogram-assisted path: capacity of the cluster-wide candidate array
 };
@@ -116,12 +111,18 @@ struct DenseAppendArgs {
   RopeTable rope;
 };
 
-struct OwnedArgs {        // sharded: owned selection list = owned sinks | owned K9 picks | owned recents
-  const int* gsel; const int* gcount; int g_stride;
+struct ShardSelectArgs {   // sharded: global selection from the gathered scores + owned list (shard.cu)
+  const float* all_score;   // [P, B, kc] all-gathered candidate scores (rank order, -inf padded)
+  const int* own_idx;       // [B, kc] this rank's candidates (global index, ascending, -1 padded)
+  int world, rank, batch, kc;
   const int* seq_len; const int* local_len; int64_t shard_start;
-  int sink, recent, k;
-  int* own_sel; int* own_count;   // [B, k] local rows, [B]
+  int k, sink, recent;
+  int* own_sel; int* own_count;   // [B, k] local rows ascending, [B]
+  const int* cand_count;          // [B] valid entries of own_idx (a prefix: the list is compacted)
 };
+constexpr int kSelCopyCtas = 16;   // CTAs per request of the one-rank (copy) selection
+__global__ void shard_select_kernel(ShardSelectArgs a);
+
 
 template <typename T, int MODE> __global__ void project_kernel(ProjectArgs a);
 template <typename T, int LG, int CPL> __global__ void latent_score_kernel(ScoreArgs a);
@@ -129,12 +130,10 @@ template <typename T, int LG, int CPL> __global__ void latent_score_kernel(Score
 // Single-CTA histogram-assisted top-k for <= 8192 entries per request (topk_cta.cu).
 cudaError_t launch_topk_cta(const TopkArgs& a, int batch, int max_entries, cudaStream_t st);
 cudaError_t launch_score_tma(const ScoreArgs& a, int batch, int max_len, cudaStream_t st, int nsm);
-__global__ void topk_cluster_kernel(TopkArgs a);
 template <int NT> __global__ void topk_hist_kernel(TopkArgs a);
 template <typename T> __global__ void recon_rope_simt_kernel(ReconArgs a);
 template <typename T, int DH, int G, bool DENSE> __global__ void flash_decode_kernel(FlashArgs a);
 template <typename T> __global__ void merge_kernel(MergeArgs a);
 template <typename T> __global__ void dense_append_kernel(DenseAppendArgs a);
-__global__ void owned_list_kernel(OwnedArgs a);
 
 }  // namespace sals

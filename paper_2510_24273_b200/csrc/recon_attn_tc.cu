@@ -453,7 +453,7 @@ sals_status launch_recon_attn_tc(const TcArgs& a, int batch, cudaStream_t st) {
     const int vhead = vq ? 128 * a.v_bits / 8 + 16 : 0;
     cuuint64_t dv[2] = {vq ? (cuuint64_t)a.v_row_bytes : (cuuint64_t)a.D, rows};
     cuuint64_t sv[1] = {vq ? (cuuint64_t)a.v_row_bytes : (cuuint64_t)a.D * 2};
-    cuuint32_t bv[2] = {vq ? (cuuint32_t)(2 * vhead) : 256u, 1};
+    cuuint32_t bv[2] = {vq ? (cuuint32_t)(2 * vhead) : 256u, 1};   // (bf16 rows: used by the v1 kernel only)
     if (g_encode(&ml, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a.latent), dl, sl, bl, estr,
                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||

@@ -26,7 +26,8 @@ EXPORTED = ["sals_workspace_bytes", "sals_append_latent", "sals_decode", "sals_d
             "sals_launch_count", "sals_profile_stage_mask", "sals_append_decode",
             "sals_append_latent_bulk", "sals_calibrate_workspace_bytes", "sals_calibrate",
             "sals_v_row_bytes", "sals_v_cache_bytes", "sals_comm_unique_id", "sals_comm_init",
-            "sals_comm_destroy", "sals_decode_sharded_workspace_bytes", "sals_decode_sharded"]
+            "sals_comm_destroy", "sals_decode_sharded_workspace_bytes", "sals_decode_sharded",
+            "sals_workspace_selection_offsets"]
 
 
 class SalsError(RuntimeError):
@@ -77,7 +78,8 @@ def _load():
         "sals_dense_workspace_bytes": (SZ, [C, I32, I32]),
         "sals_dense_decode": (I32, [C, P, P, P, I64, I32, P, I32, P, P, SZ, P]),
         "sals_shard_candidates": (I32, [C, P, P, P, I64, I32, I64, P, I32, P, P, P, P, SZ, P]),
-        "sals_shard_attend": (I32, [C, P, P, P, P, I64, I32, I64, P, I32, P, P, P, I32, P, P, SZ, P]),
+        "sals_shard_attend": (I32, [C, P, P, P, P, I64, I32, I64, P, I32, P, P, P, I32, I32, P, P, SZ, P]),
+        "sals_workspace_selection_offsets": (I32, [C, I32, I32, P, P]),
         "sals_merge_partials": (I32, [C, P, I32, I32, P, P]),
         "sals_shard_workspace_bytes": (SZ, [C, I32, I32, I32]),
         "sals_comm_unique_id": (I32, [P]),
@@ -211,11 +213,29 @@ def sals_shard_candidates(cfg, U, q, latent_shard, shard_start, local_len, max_l
 
 
 def sals_shard_attend(cfg, U, q, latent_shard, v_shard, shard_start, local_len, max_local_len, seq_len,
-                      cand_all_score, cand_all_idx, world, partial, workspace, stream=None):
+                      cand_all_score, cand_idx, world, rank, partial, workspace, stream=None):
     _check(_lib.sals_shard_attend(ctypes.byref(cfg), _p(U), _p(q), _p(latent_shard), _p(v_shard),
                                   latent_shard.shape[1], q.shape[0], int(shard_start), _p(local_len),
-                                  int(max_local_len), _p(seq_len), _p(cand_all_score), _p(cand_all_idx), int(world),
-                                  _p(partial), _p(workspace), workspace.numel(), _stream(stream)))
+                                  int(max_local_len), _p(seq_len), _p(cand_all_score), _p(cand_idx), int(world),
+                                  int(rank), _p(partial), _p(workspace), workspace.numel(), _stream(stream)))
+
+
+def sals_workspace_selection_offsets(cfg, batch, max_seq_len):
+    """Byte offsets (selection list, counts) inside a decode / shard workspace."""
+    o_sel, o_cnt = ctypes.c_size_t(0), ctypes.c_size_t(0)
+    _check(_lib.sals_workspace_selection_offsets(ctypes.byref(cfg), int(batch), int(max_seq_len),
+                                                 ctypes.byref(o_sel), ctypes.byref(o_cnt)))
+    return o_sel.value, o_cnt.value
+
+
+def shard_owned_list(cfg, workspace, batch, max_local_len):
+    """(inspection) the owned local rows [B, k] and counts [B] a completed
+    sals_shard_attend left in `workspace` (host numpy copies)."""
+    o_sel, o_cnt = sals_workspace_selection_offsets(cfg, batch, max_local_len)
+    k = cfg.top_k
+    sel = workspace[o_sel:o_sel + batch * k * 4].view(torch.int32).view(batch, k).cpu().numpy()
+    cnt = workspace[o_cnt:o_cnt + batch * 4].view(torch.int32).cpu().numpy()
+    return sel, cnt
 
 
 def sals_merge_partials(cfg, partial_all, world, batch, out, stream=None):
@@ -259,6 +279,8 @@ def sals_launch_count(reset: bool = False) -> int:
 
 
 STAGE_BITS = {"qproj_rope": 0, "score": 1, "topk": 2, "recon_attn": 3, "flash": 4, "merge": 5, "append": 6}
+EXCHANGE_BIT = 7   # (sharded) the NCCL all-gathers inside sals_decode_sharded
+SHARD_SELECT_BIT = 8   # (sharded) global selection + owned list (shard_select_kernel)
 
 
 def sals_profile_stage_mask(mask: int) -> int:

@@ -2,9 +2,11 @@
 contiguous shards of every request's tokens, two all-gathers per layer.
 
     rank p:  local q~, p' over its shard, local top-(k-x-z) candidates with
-             GLOBAL indices (sals_shard_candidates)
-    all-gather #1: (score, index) candidates -> [P, B, k]   (NCCL over NVLink)
-    rank p:  global TopK over the P*k candidates (identical on every rank),
+             GLOBAL indices, ascending (sals_shard_candidates)
+    all-gather #1: candidate SCORES only -> [P, B, k]   (NCCL over NVLink); the
+             gathered order (rank, position) is the global index order
+    rank p:  exact global TopK over the union (radix select of the (k-x-z)-th
+             score + tie quota, ranks in order) fused with its owned list,
              reconstruct + RoPE + attention over the OWNED selected tokens
              -> one (m, l, o) partial per (request, query head)   (sals_shard_attend)
     all-gather #2: partials -> [P, B, n_q, d+2]
@@ -34,7 +36,7 @@ def shard_bounds(seq_len: int, world: int, rank: int):
 class Phases:
     """Device (or oracle) implementations of the three local phases."""
     candidates: callable    # (latent_shard, start, local_len) -> (cand_score [B,k] f32, cand_idx [B,k] i32)
-    attend: callable        # (latent_shard, v_shard, start, local_len, all_score, all_idx) -> partial [B,n_q,d+2]
+    attend: callable        # (latent_shard, v_shard, start, local_len, all_score [P,B,k], own cand_idx) -> partial
     merge: callable         # (partial_all [P,B,n_q,d+2]) -> y [B, n_q*d]
 
 
@@ -55,13 +57,12 @@ class ShardedDecoder:
     def decode(self, latent_shard, v_shard, start, local_len):
         cs, ci = self.ph.candidates(latent_shard, start, local_len)
         all_s = self._gather(cs)            # [P, B, k], rank order = ascending global index
-        all_i = self._gather(ci)
-        part = self.ph.attend(latent_shard, v_shard, start, local_len, all_s, all_i)
+        part = self.ph.attend(latent_shard, v_shard, start, local_len, all_s, ci)
         part_all = self._gather(part)       # [P, B, n_q, d+2]
         return self.ph.merge(part_all)
 
 
-def gpu_phases(cfg, U, q, seq_len, max_local_len, ws, world):
+def gpu_phases(cfg, U, q, seq_len, max_local_len, ws, world, rank):
     """Phases backed by the C ABI (libsals.so) on the current CUDA stream."""
     from . import sals
     B = q.shape[0]
@@ -76,9 +77,9 @@ def gpu_phases(cfg, U, q, seq_len, max_local_len, ws, world):
         sals.sals_shard_candidates(cfg, U, q, lat, start, local_len, max_local_len, seq_len, cs, ci, ws)
         return cs, ci
 
-    def attend(lat, v, start, local_len, all_s, all_i):
-        sals.sals_shard_attend(cfg, U, q, lat, v, start, local_len, max_local_len, seq_len, all_s, all_i, world,
-                               part, ws)
+    def attend(lat, v, start, local_len, all_s, own_i):
+        sals.sals_shard_attend(cfg, U, q, lat, v, start, local_len, max_local_len, seq_len, all_s, own_i, world,
+                               rank, part, ws)
         return part
 
     def merge(part_all):
@@ -93,6 +94,7 @@ def gpu_phases(cfg, U, q, seq_len, max_local_len, ws, world):
 # ---------------------------------------------------------------------------
 def bench(args, rank, world):
     import json
+    import sys
     import time
 
     import synth
@@ -124,7 +126,7 @@ def bench(args, rank, world):
         ws = sals.alloc_workspace(sals.sals_decode_sharded_workspace_bytes(cfg, B, n_loc, world), "cuda")
         outs = [torch.empty(B, ly["q"].shape[1], dtype=ly["q"].dtype, device="cuda") for ly in layers]
     else:
-        decs = [ShardedDecoder(gpu_phases(cfg, ly["U"], ly["q"], seq, n_loc, ws, world)) for ly in layers]
+        decs = [ShardedDecoder(gpu_phases(cfg, ly["U"], ly["q"], seq, n_loc, ws, world, rank)) for ly in layers]
 
     def step():
         for i, ly in enumerate(layers):
@@ -164,6 +166,43 @@ def bench(args, rank, world):
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
+    # per-phase us per layer-step (library path): a graph of the same step with only one
+    # phase enabled (sals_profile_stage_mask), max over ranks; the phases' sum vs the step
+    # shows how much the chain overlaps
+    phases = {}
+    if comm is not None and graph is not None:
+        bits = dict(sals.STAGE_BITS)
+        bits.pop("flash", None)
+        bits.update(exchange=sals.EXCHANGE_BIT, shard_select=sals.SHARD_SELECT_BIT)
+        for name, bit in bits.items():
+            print(f"[sharded bench] phase {name}", file=sys.stderr, flush=True)
+            sals.sals_profile_stage_mask(1 << bit)
+            try:
+                with torch.cuda.stream(stream):
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=stream):
+                        step()
+            finally:
+                sals.sals_profile_stage_mask(0xffffffff)
+            with torch.cuda.stream(stream):
+                step()
+                for _ in range(3):
+                    g.replay()
+                torch.cuda.synchronize()
+                dist.barrier()
+                f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                f0.record(stream)
+                for _ in range(max(5, args.steps)):
+                    g.replay()
+                f1.record(stream)
+                torch.cuda.synchronize()
+                step()
+            pt = torch.tensor([f0.elapsed_time(f1) / max(5, args.steps)], dtype=torch.float64, device="cuda")
+            dist.all_reduce(pt, op=dist.ReduceOp.MAX)
+            us = float(pt.item()) * 1e3 / L
+            if us > 0.05:
+                phases[name] = round(us, 2)
+            del g
     if rank == 0:
         line = {"metric": "decode attention tokens/s (32-layer attention step)", "value": B / (ms / 1e3),
                 "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -174,7 +213,10 @@ def bench(args, rank, world):
                            "graph": graph is not None,
                            "exchange": "sals_decode_sharded (library NCCL)" if comm is not None
                            else "torch.distributed all_gather_into_tensor"},
-                "us_per_layer_step": ms * 1e3 / L}
+                "us_per_layer_step": ms * 1e3 / L,
+                "phases_us_per_layer": phases,
+                "phases_note": "graph of the step with one phase enabled (others skipped), max over ranks; "
+                               "'append' is the owner rank's sals_append_latent, 'exchange' the two NCCL all-gathers"}
         print(json.dumps(line), flush=True)
     if comm is not None:
         torch.cuda.synchronize()

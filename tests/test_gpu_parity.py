@@ -261,13 +261,12 @@ def test_sharded_virtual_ranks_equal_unsharded(P, sink, recent):
         ci = torch.empty(B, k, dtype=torch.int32, device="cuda")
         sals.sals_shard_candidates(cfg, U, q, lat, int(a), locd, b_ - a, seq, cs, ci, ws)
         cands_s.append(cs); cands_i.append(ci); wss.append(ws); shards.append((a, b_, lat, vv, locd))
-    all_s = torch.stack(cands_s).contiguous()
-    all_i = torch.stack(cands_i).contiguous()
+    all_s = torch.stack(cands_s).contiguous()    # the scores-only exchange
     parts = []
     for p in range(P):
         a, b_, lat, vv, locd = shards[p]
         part = torch.empty(B, sh["num_q_heads"], sh["head_dim"] + 2, dtype=torch.float32, device="cuda")
-        sals.sals_shard_attend(cfg, U, q, lat, vv, int(a), locd, b_ - a, seq, all_s, all_i, P, part, wss[p])
+        sals.sals_shard_attend(cfg, U, q, lat, vv, int(a), locd, b_ - a, seq, all_s, cands_i[p], P, p, part, wss[p])
         parts.append(part)
     out = torch.empty(B, sh["num_q_heads"] * sh["head_dim"], dtype=torch.bfloat16, device="cuda")
     sals.sals_merge_partials(cfg, torch.stack(parts).contiguous(), P, B, out)
@@ -277,6 +276,66 @@ def test_sharded_virtual_ranks_equal_unsharded(P, sink, recent):
     orc = O.decode(oc, host["U"], host["q"], host["latent"], host["v"], host["seq_len"], forced_selection=forced)
     H.check_output(H.widen(out), orc["y"], "bf16")
     assert np.max(np.abs(H.widen(out) - gpu["out"])) <= 2 ** -6
+
+
+@pytest.mark.parametrize("P,sink,recent", [(2, 0, 0), (4, 0, 0), (3, 8, 16)])
+def test_sharded_select_cross_shard_ties(P, sink, recent):
+    """Shards holding IDENTICAL latent / value rows, so every score appears P times, bitwise
+    (the per-token reduction order is shard-invariant): the scores-only exchange must split the
+    ties at the (k-x-z)-th score between the ranks exactly as the unsharded top-k does (lower
+    global index first, R5).  Checked: the union of the owned selections against the unsharded
+    GPU selection index by index, and the merged output against the oracle forced to it."""
+    from paper_2510_24273_b200 import sals
+    sh = _shape("c4", rank=256, score_rank=128, top_k=1024)
+    n1, B = 1500, 1
+    s = P * n1
+    pr = synth.gen_problem(num_q_heads=sh["num_q_heads"], num_kv_heads=sh["num_kv_heads"], head_dim=sh["head_dim"],
+                           rank=sh["rank"], batch=B, seq_lens=[n1], cap=n1, seed=43)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda().bfloat16()
+    U, q = dev(pr["U"]), dev(pr["q"])
+    lat = dev(np.concatenate([pr["latent"]] * P, axis=1))
+    vv = dev(np.concatenate([pr["v"]] * P, axis=1))
+    cfg = sals.make_config(**sh, sink=sink, recent=recent)
+    seq = torch.full((B,), s, dtype=torch.int32, device="cuda")
+    k = sh["top_k"]
+    ws = sals.alloc_workspace(sals.sals_workspace_bytes(cfg, B, s), "cuda")
+    ref_out = torch.empty(B, sh["num_q_heads"] * sh["head_dim"], dtype=torch.bfloat16, device="cuda")
+    ref_sel = torch.full((B, k), -7, dtype=torch.int32, device="cuda")
+    sals.sals_decode(cfg, U, q, lat, vv, seq, s, ref_out, ws, sel_idx_out=ref_sel)
+    cands_s, cands_i, wss = [], [], []
+    for p in range(P):
+        a = p * n1
+        locd = torch.full((B,), n1, dtype=torch.int32, device="cuda")
+        w = sals.alloc_workspace(sals.sals_shard_workspace_bytes(cfg, B, n1, P), "cuda")
+        cs = torch.empty(B, k, dtype=torch.float32, device="cuda")
+        ci = torch.empty(B, k, dtype=torch.int32, device="cuda")
+        sals.sals_shard_candidates(cfg, U, q, lat[:, a:a + n1].contiguous(), a, locd, n1, seq, cs, ci, w)
+        cands_s.append(cs); cands_i.append(ci); wss.append(w)
+    all_s = torch.stack(cands_s).contiguous()
+    owned, parts = [], []
+    for p in range(P):
+        a = p * n1
+        locd = torch.full((B,), n1, dtype=torch.int32, device="cuda")
+        part = torch.empty(B, sh["num_q_heads"], sh["head_dim"] + 2, dtype=torch.float32, device="cuda")
+        sals.sals_shard_attend(cfg, U, q, lat[:, a:a + n1].contiguous(), vv[:, a:a + n1].contiguous(), a, locd, n1,
+                               seq, all_s, cands_i[p], P, p, part, wss[p])
+        torch.cuda.synchronize()
+        parts.append(part)
+        own, cnt = sals.shard_owned_list(cfg, wss[p], B, n1)   # (debug view of the workspace)
+        owned.append(own[0, :cnt[0]].astype(np.int64) + a)
+    out = torch.empty_like(ref_out)
+    sals.sals_merge_partials(cfg, torch.stack(parts).contiguous(), P, B, out)
+    torch.cuda.synchronize()
+    gsel = ref_sel[0].cpu().numpy()
+    gsel = gsel[gsel >= 0].astype(np.int64)
+    np.testing.assert_array_equal(np.concatenate(owned), gsel)
+    assert np.max(np.abs(H.widen(out) - H.widen(ref_out))) <= 2 ** -6
+    oc = H.oracle_cfg(sh, sink, recent)
+    full_lat = np.concatenate([pr["latent"]] * P, axis=1)
+    full_v = np.concatenate([pr["v"]] * P, axis=1)
+    orc = O.decode(oc, H.widen(U), H.widen(q), H.widen(dev(full_lat)), H.widen(dev(full_v)), np.array([s]),
+                   forced_selection=[gsel])
+    H.check_output(H.widen(out), orc["y"], "bf16")
 
 
 @pytest.mark.parametrize("sink,recent", [(0, 0), (16, 64)])

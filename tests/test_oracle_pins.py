@@ -326,6 +326,18 @@ def test_sharded_selection_and_merge_equal_unsharded():
             ci.append(x2)
         got = O.global_select(np.concatenate(cs), np.concatenate(ci), s, cfg)
         np.testing.assert_array_equal(got, ref)
+        # scores-only exchange: each rank's owned part from the gathered scores, union == ref
+        y = cfg.top_k - cfg.sink - cfg.recent
+        pad = max(cfg.top_k, 1)
+        gs, gi = np.full((P, pad), -np.inf), np.full((P, pad), -1)
+        for p_ in range(P):
+            a, b = bounds[p_], bounds[p_ + 1]
+            keep = (ci[p_] >= cfg.sink) & (ci[p_] < s - cfg.recent)
+            sel = np.sort(ci[p_][keep][np.lexsort((ci[p_][keep], -cs[p_][keep]))[:y]])   # ranked, ascending index
+            gs[p_, :len(sel)] = sc[sel]
+            gi[p_, :len(sel)] = sel
+        owned = [O.shard_owned_selection(gs, gi[p_], p_, bounds[p_], bounds[p_ + 1], s, cfg) for p_ in range(P)]
+        np.testing.assert_array_equal(np.concatenate(owned), ref)
         # LSE merge of per-shard partial attention == restricted attention over all of C
         qR = rng.standard_normal((cfg.num_q_heads, cfg.head_dim))
         KR = rng.standard_normal((len(ref), cfg.num_kv_heads, cfg.head_dim))

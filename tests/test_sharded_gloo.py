@@ -49,15 +49,13 @@ def oracle_phases(cfg, U, q, s):
             ci[b, : len(sel)] = torch.from_numpy(sel.astype(np.int32))
         return cs, ci
 
-    def attend(lat, v, start, local_len, all_s, all_i):
+    def attend(lat, v, start, local_len, all_s, own_i):
+        rank = dist.get_rank()
         part = torch.zeros(B, nq, d + 2, dtype=torch.float64)
         for b in range(B):
             n = int(local_len[b])
-            flat_s = all_s[:, b].reshape(-1).double().numpy()
-            flat_i = all_i[:, b].reshape(-1).numpy().astype(np.int64)
-            valid = flat_i >= 0
-            gsel = O.global_select(flat_s[valid], flat_i[valid], s, cfg)
-            own = gsel[(gsel >= start) & (gsel < start + n)]
+            own = O.shard_owned_selection(all_s[:, b].double().numpy(), own_i[b].numpy().astype(np.int64), rank,
+                                          start, start + n, s, cfg)
             loc = own - start
             KC = O.reconstruct(lat[b, loc], U).reshape(len(loc), nkv, d)
             KR = O.rope(KC, own[:, None], cfg.rope_base)
