@@ -155,11 +155,15 @@ sals_status sals_decode(const sals_config* cfg, const void* U, const void* q,
  *   latent_cache[b, start + i, :] = U^T k[b, i, :],  v_cache[b, start + i, :] = v[b, i, :]
  *   k, v    [B, n_tokens, D]  PRE-RoPE keys / values (device)
  *   start   host: slot of token 0 (the same for every request), start + n_tokens <= cap
- * A plain dense GEMM (no fused epilogue): cuBLAS (bf16 in, fp32 accumulate,
- * rounded to dtype), written straight into the cache rows.  Uses a cuBLAS
- * handle created on the calling thread's first call (the only state the
- * library keeps besides the comm handle).  Not CUDA-graph captured by the tests.
- * Value rows are copied as dtype: SALS_ERR_UNSUPPORTED with cfg->v_bits 4 / 2.
+ * bf16 with D and r multiples of 64: the in-build tcgen05 GEMM (TMA-fed, fp32
+ * accumulation in TMEM, rounded to bf16 in the epilogue), written straight into
+ * the cache rows; other shapes / fp32: cuBLAS (fp32 accumulate) with a cuBLAS
+ * handle created on the calling thread's first call per device.
+ * Value rows: copied as dtype, or with cfg->v_bits 4 / 2 (bf16, head_dim 128)
+ * quantised per token exactly as sals_append_latent does (R15: codes, bf16 scale
+ * and zero), and with recent = w > 0 the LAST w tokens of the block also written
+ * into the 8-bit recent-window ring (slot pos % w; call with the cache's
+ * allocation batch, as for the other calls).
  */
 sals_status sals_append_latent_bulk(const sals_config* cfg, const void* U, const void* k, const void* v,
                                     int32_t batch, int32_t n_tokens, int64_t start, void* latent_cache,

@@ -656,7 +656,8 @@ sals_status sals_decode(const sals_config* cfg, const void* U, const void* q, co
 }
 
 int sals_prefill_impl(const sals_config* cfg, const void* U, const void* k, const void* v, int32_t batch,
-                      int32_t n_tokens, int64_t start, void* latent_cache, void* v_cache, int64_t cap, void* stream);
+                      int32_t n_tokens, int64_t start, void* latent_cache, void* v_cache, int64_t cap, void* stream,
+                      int do_latent, int do_v);
 const char* sals_prefill_last_error(void);
 
 size_t sals_calibrate_ws_impl(int D);
@@ -688,8 +689,24 @@ sals_status sals_append_latent_bulk(const sals_config* cfg, const void* U, const
   if (!U || !k || !v || !latent_cache || !v_cache) return fail(SALS_ERR_INVALID_ARGUMENT, "NULL tensor argument");
   if (batch < 1 || n_tokens < 1 || cap < 1 || start < 0 || start + n_tokens > cap)
     return fail(SALS_ERR_INVALID_ARGUMENT, "need batch, n_tokens >= 1 and 0 <= start, start + n_tokens <= cap");
-  if (vq_bits(cfg)) return fail(SALS_ERR_UNSUPPORTED, "bulk append writes dtype value rows (v_bits 0 / 16 only)");
-  if (sals_prefill_impl(cfg, U, k, v, batch, n_tokens, start, latent_cache, v_cache, cap, stream) != 0)
+  if (vq_bits(cfg) && (cfg->dtype != SALS_BF16 || cfg->head_dim != 128))
+    return fail(SALS_ERR_UNSUPPORTED, "quantised value rows need bf16 and head_dim 128");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  // latent rows: the tcgen05 GEMM (prefill_tc.cu), cuBLAS outside its shapes
+  cudaError_t e = launch_prefill_tc(cfg, U, k, batch, n_tokens, start, latent_cache, cap, st);
+  if (e != cudaSuccess && e != cudaErrorNotSupported) return fail(SALS_ERR_CUDA, "prefill_tc: %s", cudaGetErrorString(e));
+  const bool latent_done = e == cudaSuccess;
+  if (latent_done) g_launches.fetch_add(1, std::memory_order_relaxed);
+  // value rows: quantised in a kernel (the append's rule), else copied by the fallback
+  if (vq_bits(cfg)) {
+    e = launch_prefill_vq(cfg, v, batch, n_tokens, start, v_cache, cap, (int)v_row_bytes(cfg), hp_window(cfg),
+                          (int64_t)batch * cap * (int64_t)v_row_bytes(cfg), st);
+    if (e != cudaSuccess) return fail(SALS_ERR_CUDA, "prefill_vq: %s", cudaGetErrorString(e));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  if ((!latent_done || !vq_bits(cfg)) &&
+      sals_prefill_impl(cfg, U, k, v, batch, n_tokens, start, latent_cache, v_cache, cap, stream, latent_done ? 0 : 1,
+                        vq_bits(cfg) ? 0 : 1) != 0)
     return fail(SALS_ERR_CUDA, "%s", sals_prefill_last_error());
   return SALS_OK;
 }

@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include "common.cuh"
+#include "sals.h"
 
 namespace sals {
 
@@ -120,6 +121,10 @@ struct ShardSelectArgs {   // sharded: global selection from the gathered scores
   int* own_sel; int* own_count;   // [B, k] local rows ascending, [B]
   const int* cand_count;          // [B] valid entries of own_idx (a prefix: the list is compacted)
 };
+cudaError_t launch_prefill_tc(const sals_config* c, const void* U, const void* k, int batch, int n, int64_t start,
+                              void* latent, int64_t cap, cudaStream_t st);
+cudaError_t launch_prefill_vq(const sals_config* c, const void* v, int batch, int n, int64_t start, void* v_cache,
+                              int64_t cap, int v_row_bytes, int hp_window, int64_t hp_ring_off, cudaStream_t st);
 constexpr int kSelCopyCtas = 16;   // CTAs per request of the one-rank (copy) selection
 __global__ void shard_select_kernel(ShardSelectArgs a);
 

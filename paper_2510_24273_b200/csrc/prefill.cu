@@ -2,11 +2,11 @@
 // applied to a block of n consecutive tokens of every request:
 //   latent_cache[b, start + i, :] = U^T k[b, i, :]      (i < n)
 //   v_cache[b, start + i, :]      = v[b, i, :]
-// The projection is a plain dense GEMM (B*n x D) x (D x r) with no fused
-// epilogue, so it runs on cuBLAS (bf16 in, fp32 accumulate, output written
-// straight into the cache rows: one strided-batched call, the batch stride is
-// the cache's request pitch); the value rows are one 2-D async copy.  Not on
-// the decode hot path.
+// bf16 with D, r multiples of 64 runs on the in-build tcgen05 GEMM
+// (prefill_tc.cu); this file is the fallback for the other shapes / fp32: a
+// cuBLAS strided-batched GEMM (fp32 accumulate, written straight into the cache
+// rows, the batch stride is the cache's request pitch) and the dtype value rows
+// as one 2-D async copy.  Not on the decode hot path.
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
 
@@ -41,11 +41,12 @@ extern "C" const char* sals_prefill_last_error(void) { return g_prefill_err.c_st
 // (api.cu maps the code to a sals_status).
 extern "C" int sals_prefill_impl(const sals_config* cfg, const void* U, const void* k, const void* v, int32_t batch,
                                  int32_t n_tokens, int64_t start, void* latent_cache, void* v_cache, int64_t cap,
-                                 void* stream) {
+                                 void* stream, int do_latent, int do_v) {
   const int D = cfg->num_kv_heads * cfg->head_dim, r = cfg->rank;
   const bool bf16 = cfg->dtype == SALS_BF16;
   const size_t es = bf16 ? 2 : 4;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (do_latent) {
   cublasHandle_t hb = cublas_handle();
   if (!hb) {
     g_prefill_err = "cublasCreate failed";
@@ -66,6 +67,8 @@ extern "C" int sals_prefill_impl(const sals_config* cfg, const void* U, const vo
     g_prefill_err = "cublasGemmStridedBatchedEx failed (" + std::to_string((int)cs) + ")";
     return 1;
   }
+  }
+  if (!do_v) return 0;
   cudaError_t e = cudaMemcpy2DAsync(reinterpret_cast<char*>(v_cache) + (size_t)start * D * es, (size_t)cap * D * es,
                                     v, (size_t)n_tokens * D * es, (size_t)n_tokens * D * es, batch,
                                     cudaMemcpyDeviceToDevice, st);

@@ -13,6 +13,7 @@
 // the result is deterministic and needs no global workspace or atomics.
 #include "common.cuh"
 #include "kernels.h"
+#include "quant.cuh"
 
 namespace sals {
 
@@ -139,13 +140,9 @@ project_kernel(ProjectArgs a) {
                                   (((size_t)b * a.cap + pb) * a.D) * sizeof(T) + v * 16) = val;
       }
     } else {
-      // ---- append with channel-wise group quantisation (DESIGN R15): four
-      // lanes per 32-channel group (8 channels each, one 16-byte load), min / max by
-      // two shuffles; zero = min, scale = (max-min)/qmax, both rounded to bf16 first,
-      // codes from the rounded values, packed low bits first.  R15's code rule is
-      // exact IEEE fp32 (the oracle takes the same decisions): one rounded subtract,
-      // one rounded divide (no reciprocal), round half to even, clamp
-      const int bits = a.v_bits, qmax = (1 << bits) - 1;
+      // ---- append with channel-wise group quantisation (DESIGN R15; quant.cuh):
+      // four lanes per 32-channel group, 8 channels (one 16-byte load) each
+      const int bits = a.v_bits;
       const int gph = 128 / 32;                       // groups per head (head_dim 128)
       const int hb = 128 * bits / 8 + gph * 4;        // bytes per head in a row
       const int nitems = a.B * (a.D / 8);             // (request, 8-channel slice); 4 per group, lane-adjacent
@@ -157,45 +154,13 @@ project_kernel(ProjectArgs a) {
         float f[8];
         if (ok) Elem<__nv_bfloat16>::unpack(ld_v4(reinterpret_cast<const char*>(a.v_new) + ((size_t)b * a.D + sl * 8) * 2), f);
         else for (int e = 0; e < 8; ++e) f[e] = 0.f;
-        float lo = f[0], hi = f[0];
-#pragma unroll
-        for (int e = 1; e < 8; ++e) { lo = fminf(lo, f[e]); hi = fmaxf(hi, f[e]); }
-        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 1)); hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, 1));
-        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 2)); hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, 2));
-        if (!ok) continue;
-        const __nv_bfloat16 zb = __float2bfloat16_rn(lo);
-        const __nv_bfloat16 sb = __float2bfloat16_rn(__fdiv_rn(__fsub_rn(hi, lo), (float)qmax));
-        const float zf = __bfloat162float(zb), sf = __bfloat162float(sb);
-        uint32_t w = 0;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int c = sf > 0.f ? min(qmax, max(0, __float2int_rn(__fdiv_rn(__fsub_rn(f[e], zf), sf)))) : 0;
-          w |= (uint32_t)c << (e * bits);
-        }
-        const int pb = a.pos ? a.pos[b] : a.seq_len[b] - 1;
+        const int pb = ok ? (a.pos ? a.pos[b] : a.seq_len[b] - 1) : 0;
         char* row = reinterpret_cast<char*>(a.v_cache) + ((size_t)b * a.cap + pb) * a.v_row_bytes + (size_t)h * hb;
-        if (bits == 4) *reinterpret_cast<uint32_t*>(row + gq * 16 + q * 4) = w;
-        else *reinterpret_cast<uint16_t*>(row + gq * 8 + q * 2) = (uint16_t)w;
-        if (q == 0)
-          *reinterpret_cast<uint32_t*>(row + 128 * bits / 8 + gq * 4) =
-              (uint32_t)__bfloat16_as_ushort(sb) | ((uint32_t)__bfloat16_as_ushort(zb) << 16);
-        if (a.hp_window > 0) {
-          // high-precision copy of the recent window: 8 bits in ring slot pos % w
-          const __nv_bfloat16 s8 = __float2bfloat16_rn(__fdiv_rn(__fsub_rn(hi, lo), 255.f));
-          const float s8f = __bfloat162float(s8);
-          uint32_t w8[2] = {0, 0};
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int c = s8f > 0.f ? min(255, max(0, __float2int_rn(__fdiv_rn(__fsub_rn(f[e], zf), s8f)))) : 0;
-            w8[e >> 2] |= (uint32_t)c << ((e & 3) * 8);
-          }
-          char* ring = reinterpret_cast<char*>(a.v_cache) + a.hp_ring_off +
-                       ((size_t)b * a.hp_window + pb % a.hp_window) * (size_t)(a.D / 128) * 144 + (size_t)h * 144;
-          *reinterpret_cast<uint2*>(ring + gq * 32 + q * 8) = make_uint2(w8[0], w8[1]);
-          if (q == 0)
-            *reinterpret_cast<uint32_t*>(ring + 128 + gq * 4) =
-                (uint32_t)__bfloat16_as_ushort(s8) | ((uint32_t)__bfloat16_as_ushort(zb) << 16);
-        }
+        char* ring = a.hp_window > 0
+                         ? reinterpret_cast<char*>(a.v_cache) + a.hp_ring_off +
+                               ((size_t)b * a.hp_window + pb % a.hp_window) * (size_t)(a.D / 128) * 144 + (size_t)h * 144
+                         : nullptr;
+        quantize_slice(f, ok, bits, row, gq, q, ring);
       }
     }
   }

@@ -434,6 +434,70 @@ def test_append_latent_bulk(dtype):
     assert bool((vc[:, :start] == 7.0).all()) and bool((vc[:, start + n:] == 7.0).all())
 
 
+@pytest.mark.parametrize("nkv,r,B,n,start", [(32, 512, 2, 1000, 3000), (8, 512, 1, 4096, 0), (8, 256, 3, 77, 5)])
+def test_append_latent_bulk_tcgen05(nkv, r, B, n, start):
+    """The tcgen05 bulk-append GEMM (prefill_tc.cu) at model sizes (D = 4096 / 1024, r = 512,
+    ragged n): latent rows == U^T k (fp64 oracle, one bf16 rounding + fp32-accumulation
+    allowance), rows outside the block untouched."""
+    from paper_2510_24273_b200 import sals
+    d = 128
+    D = nkv * d
+    sh = dict(num_q_heads=nkv, num_kv_heads=nkv, head_dim=d, rank=r, score_rank=r // 2, top_k=128, rope_base=1e4,
+              dtype="bf16")
+    cfg = sals.make_config(**sh)
+    rng = np.random.default_rng(11)
+    cap = start + n + 50
+    U = torch.from_numpy(synth.orthonormal(rng, D, r)).cuda().bfloat16()
+    k = torch.from_numpy(rng.normal(size=(B, n, D))).cuda().bfloat16()
+    v = torch.from_numpy(rng.normal(size=(B, n, D))).cuda().bfloat16()
+    lat = torch.full((B, cap, r), 7.0, dtype=torch.bfloat16, device="cuda")
+    vc = torch.full((B, cap, D), 7.0, dtype=torch.bfloat16, device="cuda")
+    sals.sals_launch_count(reset=True)
+    sals.sals_append_latent_bulk(cfg, U, k, v, start, lat, vc)
+    torch.cuda.synchronize()
+    assert sals.sals_launch_count(reset=True) >= 1          # the in-build kernel ran (no cuBLAS fallback)
+    ref = O.project_latent(H.widen(U), H.widen(k).reshape(B * n, D)).reshape(B, n, r)
+    got = H.widen(lat[:, start:start + n])
+    tol = 2.0 ** -7 * np.abs(ref) + 2e-3
+    assert np.all(np.abs(got - ref) <= tol), np.max(np.abs(got - ref) - tol)
+    assert torch.equal(vc[:, start:start + n], v)
+    assert bool((lat[:, :start] == 7.0).all()) and bool((lat[:, start + n:] == 7.0).all())
+
+
+@pytest.mark.parametrize("bits,z", [(4, 0), (2, 0), (4, 64), (2, 100)])
+def test_append_latent_bulk_quantized(bits, z):
+    """Bulk prefill of a quantised value cache: every row of the block BYTE-identical to
+    the oracle's quantiser (R15), the 8-bit recent-window ring holding the last z tokens of
+    the block at slot pos % z, rows outside the block untouched."""
+    from paper_2510_24273_b200 import sals
+    nkv, d, r, B, n, start = 8, 128, 256, 2, 700, 40
+    D = nkv * d
+    sh = dict(num_q_heads=nkv * 4, num_kv_heads=nkv, head_dim=d, rank=r, score_rank=128, top_k=256, rope_base=1e6,
+              dtype="bf16")
+    cfg = sals.make_config(**sh, v_bits=bits, recent=z)
+    rng = np.random.default_rng(13)
+    cap = start + n + 9
+    U = torch.from_numpy(synth.orthonormal(rng, D, r)).cuda().bfloat16()
+    k = torch.from_numpy(rng.normal(size=(B, n, D))).cuda().bfloat16()
+    v = torch.from_numpy(rng.normal(size=(B, n, D))).cuda().bfloat16()
+    lat = torch.zeros(B, cap, r, dtype=torch.bfloat16, device="cuda")
+    rb = sals.sals_v_row_bytes(cfg)
+    total = sals.sals_v_cache_bytes(cfg, B, cap)
+    vq = torch.full((total,), 0xA5, dtype=torch.uint8, device="cuda")
+    sals.sals_append_latent_bulk(cfg, U, k, v, start, lat, vq)
+    torch.cuda.synchronize()
+    rows = vq[:B * cap * rb].view(B, cap, rb).cpu().numpy()
+    vh = H.widen(v)
+    np.testing.assert_array_equal(rows[:, start:start + n], _pack_values(vh, bits, nkv))
+    assert (rows[:, :start] == 0xA5).all() and (rows[:, start + n:] == 0xA5).all()
+    if z:
+        ring = vq[B * cap * rb:].view(B, z, nkv * 144).cpu().numpy()
+        for b in range(B):
+            for t in range(n - z, n):
+                pos = start + t
+                np.testing.assert_array_equal(ring[b, pos % z], _pack8(vh[b, t][None], nkv)[0])
+
+
 # ------------------------------------------------------------------ calibration
 def test_calibrate_matches_oracle():
     """sals_calibrate (cuBLAS Gram + cuSOLVER syevd, fp32) == oracle calibrate (fp64
