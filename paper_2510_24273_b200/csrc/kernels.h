@@ -12,7 +12,6 @@
 namespace sals {
 
 // Block sizes shared by kernels and launcher.
-constexpr int kProjThreads = 256;
 constexpr int kScoreThreads = 256;
 // First radix digit of the top-k, built by the score kernel: the top 11 bits of
 // the order-preserving float key of every ranked score.
@@ -129,7 +128,7 @@ constexpr int kSelCopyCtas = 16;   // CTAs per request of the one-rank (copy) se
 __global__ void shard_select_kernel(ShardSelectArgs a);
 
 
-template <typename T, int MODE> __global__ void project_kernel(ProjectArgs a);
+template <typename T, int MODE, int NT> __global__ void project_kernel(ProjectArgs a);
 template <typename T, int LG, int CPL> __global__ void latent_score_kernel(ScoreArgs a);
 // TMA-streamed bf16 scoring (score_tma.cu); cudaErrorNotSupported outside its shapes.
 // Single-CTA histogram-assisted top-k for <= 8192 entries per request (topk_cta.cu).

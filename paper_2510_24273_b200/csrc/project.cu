@@ -17,7 +17,13 @@
 
 namespace sals {
 
-constexpr int kProjWarps = kProjThreads / 32;
+#ifdef SALS_TC_TRACE
+__device__ unsigned long long g_proj_trace[16];
+#define PJ_STAMP(i) do { if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) g_proj_trace[(i)] = clock64(); } while (0)
+#else
+#define PJ_STAMP(i) do {} while (0)
+#endif
+
 constexpr int kProjBT = 8;        // requests per pass
 constexpr int kProjMaxRows = 512; // rows per CTA (D / CS)
 constexpr int kProjUnroll = 8;    // row loads in flight per lane
@@ -28,8 +34,9 @@ constexpr int kProjUnroll = 8;    // row loads in flight per lane
 // MODE 0: append (k~ = U^T k_new -> latent row, v row copy); 1: query projection
 // (+ query RoPE role, histogram zeroing); 2: both in one launch (sals_append_decode):
 // blockIdx.y < n_append_blocks are append column blocks, the rest the query role.
-template <typename T, int MODE>
-__global__ void __launch_bounds__(kProjThreads, SALS_PROJ_MINB)   // 2: <= 128 registers, co-resident with the next kernel
+// NT threads: 512 when a CTA owns 512 rows of U (D = 4096), else 256 (measured)
+template <typename T, int MODE, int NT>
+__global__ void __launch_bounds__(NT, SALS_PROJ_MINB)   // 2: <= 128 registers, co-resident with the next kernel
 project_kernel(ProjectArgs a) {
   const bool pool = MODE == 1 || (MODE == 2 && (int)blockIdx.y >= a.n_append_blocks);
   const int yb = (MODE == 2 && pool) ? (int)blockIdx.y - a.n_append_blocks : (int)blockIdx.y;   // block within the role
@@ -38,7 +45,7 @@ project_kernel(ProjectArgs a) {
   constexpr int EPC = Elem<T>::kPer16;       // columns per lane
   constexpr int CPB = 8 * EPC;               // columns per CTA
   __shared__ float xs[kProjBT][kProjMaxRows];
-  __shared__ float wred[kProjWarps][kProjBT][CPB];
+
   __shared__ float cred[kProjBT][CPB];
   __shared__ float incoming[kProjBT * CPB];   // [source rank][owned output] partials pushed by peers
   const int CS = (int)cluster_nctarank();
@@ -61,12 +68,15 @@ project_kernel(ProjectArgs a) {
   // (rows [row0, row1) x its CPB columns, 128 B per row) is copied into shared
   // memory by cp.async BEFORE waiting on the upstream grid, so no U load is left
   // on the critical path after the wait, whatever the rows per CTA.
-  extern __shared__ __align__(16) uint8_t sU[];   // [rows_per][128 B]
+  extern __shared__ __align__(16) uint8_t sU[];   // [rows_per][128 B], then wred
+  // per-warp partial outputs [NT / 32][kProjBT][CPB] (dynamic: 32 KB at 16 warps)
+  float (*wred)[kProjBT][CPB] = reinterpret_cast<float (*)[kProjBT][CPB]>(sU + (size_t)a.rows_per_cta * 128);
   const int base0 = row0 + 4 * warp + slot;
+  PJ_STAMP(0);
   if (!rope_role) {
     const int nvec = (row1 - row0) * 8;
     const uint32_t su = smem_u32(sU);
-    for (int i = tid; i < nvec; i += kProjThreads) {
+    for (int i = tid; i < nvec; i += NT) {
       const int rr = i >> 3, cv = i & 7;
       const int cc = yb * CPB + cv * EPC;
       const bool okc = cc < ncols;
@@ -78,10 +88,12 @@ project_kernel(ProjectArgs a) {
   }
   __shared__ float2 sth[128];   // (th_hi, th_lo) per rotation pair: indexed per lane, so not from param space
   if (rope_role)
-    for (int i = tid; i < a.rope.half; i += kProjThreads) sth[i] = make_float2(a.rope.th_hi[i], a.rope.th_lo[i]);
+    for (int i = tid; i < a.rope.half; i += NT) sth[i] = make_float2(a.rope.th_hi[i], a.rope.th_lo[i]);
   __syncthreads();
 
+  PJ_STAMP(1);
   pdl_wait();
+  PJ_STAMP(2);
   // Dependents may launch now: their pre-wait sections only read weights (U) and
   // the latent rows of earlier steps / of the sals_append_latent that this
   // grid's griddepcontrol.wait has just seen complete (PDL).
@@ -92,17 +104,17 @@ project_kernel(ProjectArgs a) {
     const int half = a.rope.half, d = 2 * half;
     const int nq = a.n_q;
     if (a.hist0_zero)   // the score kernel accumulates the top-digit histogram into this
-      for (int i = rank * kProjThreads + tid; i < a.hist0_words; i += CS * kProjThreads) a.hist0_zero[i] = 0u;
+      for (int i = rank * NT + tid; i < a.hist0_words; i += CS * NT) a.hist0_zero[i] = 0u;
     // (request, head, pair) tasks split over the CS CTAs of this row; loads of 8
     // tasks are issued before any math so the latency is paid once per batch
     const int per_req = half * nq;
     const int total = a.B * per_req;
-    for (int t0 = rank * kProjThreads + tid; t0 < total; t0 += CS * kProjThreads * 8) {
+    for (int t0 = rank * NT + tid; t0 < total; t0 += CS * NT * 8) {
       float xl[8], xh[8];
       int lo_[8], hi_[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int t = t0 + u * CS * kProjThreads;
+        const int t = t0 + u * CS * NT;
         xl[u] = xh[u] = 0.f;
         if (t < total) {
           const int b = t / per_req, r = t % per_req, p = r % half, h = r / half;
@@ -113,7 +125,7 @@ project_kernel(ProjectArgs a) {
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int t = t0 + u * CS * kProjThreads;
+        const int t = t0 + u * CS * NT;
         if (t < total) {
           const int b = t / per_req, r = t % per_req, p = r % half, h = r / half;
           float c, s; rope_cs_fast(sth[p].x, sth[p].y, a.seq_len[b] - 1, c, s);
@@ -132,7 +144,7 @@ project_kernel(ProjectArgs a) {
     if (a.v_bits == 0) {
       // ---- append: copy v_new[b] -> v_cache[b, pos_b] (16-byte vectors) ----
       const int nvec = a.D * (int)sizeof(T) / 16;
-      for (int i = cta * kProjThreads + tid; i < a.B * nvec; i += ncta * kProjThreads) {
+      for (int i = cta * NT + tid; i < a.B * nvec; i += ncta * NT) {
         const int b = i / nvec, v = i % nvec;
         const uint4 val = ld_v4(reinterpret_cast<const char*>(a.v_new) + ((size_t)b * a.D) * sizeof(T) + v * 16);
         const int pb = a.pos ? a.pos[b] : a.seq_len[b] - 1;
@@ -146,7 +158,7 @@ project_kernel(ProjectArgs a) {
       const int gph = 128 / 32;                       // groups per head (head_dim 128)
       const int hb = 128 * bits / 8 + gph * 4;        // bytes per head in a row
       const int nitems = a.B * (a.D / 8);             // (request, 8-channel slice); 4 per group, lane-adjacent
-      for (int i0 = cta * kProjThreads; i0 < nitems; i0 += ncta * kProjThreads) {
+      for (int i0 = cta * NT; i0 < nitems; i0 += ncta * NT) {
         const int i = i0 + tid;
         const bool ok = i < nitems;
         const int b = ok ? i / (a.D / 8) : 0, sl = ok ? i - b * (a.D / 8) : 0;
@@ -171,7 +183,7 @@ project_kernel(ProjectArgs a) {
     // 16-byte vector per thread per head, all loads issued before the sums
     {
       const int nvec_row = (row1 - row0) / EPC;          // rows_per is a multiple of EPC
-      for (int i = tid; i < kProjBT * nvec_row; i += kProjThreads) {
+      for (int i = tid; i < kProjBT * nvec_row; i += NT) {
         const int bb = i / nvec_row, cv = i - bb * nvec_row;
         const int c = row0 + cv * EPC;
         float v[EPC];
@@ -197,6 +209,7 @@ project_kernel(ProjectArgs a) {
     }
     if (b0 == 0) asm volatile("cp.async.wait_all;" ::: "memory");   // this thread's U copies
     __syncthreads();                                                  // everyone's copies and xs visible
+    PJ_STAMP(3);
 
     float acc[kProjBT][EPC];
 #pragma unroll
@@ -204,43 +217,56 @@ project_kernel(ProjectArgs a) {
 #pragma unroll
       for (int e = 0; e < EPC; ++e) acc[bb][e] = 0.f;
     if (col_ok) {
-      // rows handled by this lane: base0 + 32 i, from the shared-memory copy of U
+      // rows handled by this lane: base0 + 32 i, from the shared-memory copy of U;
+      // packed FFMA2 over column pairs (half the FMA-pipe issue slots)
       auto fma_row = [&](const uint4& raw, int c) {
         float uf[EPC];
         Elem<T>::unpack(raw, uf);
 #pragma unroll
         for (int bb = 0; bb < kProjBT; ++bb) {
           const float xv = xs[bb][c - row0];
+          const float2 x2 = make_float2(xv, xv);
 #pragma unroll
-          for (int e = 0; e < EPC; ++e) acc[bb][e] = fmaf(uf[e], xv, acc[bb][e]);
+          for (int e = 0; e < EPC; e += 2) {
+            const float2 r2 = __ffma2_rn(make_float2(uf[e], uf[e + 1]), x2, make_float2(acc[bb][e], acc[bb][e + 1]));
+            acc[bb][e] = r2.x;
+            acc[bb][e + 1] = r2.y;
+          }
         }
       };
 #pragma unroll 4
-      for (int c = base0; c < row1; c += 4 * kProjWarps)
+      for (int c = base0; c < row1; c += 4 * (NT / 32))
         fma_row(*reinterpret_cast<const uint4*>(sU + (c - row0) * 128 + cl * 16), c);
     }
-    // reduce the 4 row slots of the warp (lanes cl, cl+8, cl+16, cl+24)
+    PJ_STAMP(4);
+    // reduce the 4 row slots of the warp (lanes cl, cl+8, cl+16, cl+24), transposed:
+    // each exchange halves the values a lane keeps (48 shuffles instead of 128), and
+    // every lane ends with 2 requests x EPC columns summed over the 4 slots
+    {
+      const int s1 = (lane >> 4) & 1, s0 = (lane >> 3) & 1;
+      float k1[kProjBT / 2][EPC];
 #pragma unroll
-    for (int bb = 0; bb < kProjBT; ++bb)
+      for (int bq = 0; bq < kProjBT / 2; ++bq)
 #pragma unroll
-      for (int e = 0; e < EPC; ++e) {
-        float v = acc[bb][e];
-        v += __shfl_xor_sync(0xffffffffu, v, 8);
-        v += __shfl_xor_sync(0xffffffffu, v, 16);
-        acc[bb][e] = v;
-      }
-    if (slot == 0) {
+        for (int e = 0; e < EPC; ++e) {
+          const float lo = acc[bq][e], hi = acc[bq + kProjBT / 2][e];
+          k1[bq][e] = (s1 ? hi : lo) + __shfl_xor_sync(0xffffffffu, s1 ? lo : hi, 16);
+        }
 #pragma unroll
-      for (int bb = 0; bb < kProjBT; ++bb)
+      for (int bq = 0; bq < kProjBT / 4; ++bq)
 #pragma unroll
-        for (int e = 0; e < EPC; ++e) wred[warp][bb][cl * EPC + e] = acc[bb][e];
+        for (int e = 0; e < EPC; ++e) {
+          const float lo = k1[bq][e], hi = k1[bq + kProjBT / 4][e];
+          const float v = (s0 ? hi : lo) + __shfl_xor_sync(0xffffffffu, s0 ? lo : hi, 8);
+          wred[warp][(kProjBT / 2) * s1 + (kProjBT / 4) * s0 + bq][cl * EPC + e] = v;
+        }
     }
     __syncthreads();
-    for (int i = tid; i < kProjBT * CPB; i += kProjThreads) {
+    for (int i = tid; i < kProjBT * CPB; i += NT) {
       const int bb = i / CPB, j = i % CPB;
       float s = 0.f;
 #pragma unroll
-      for (int w = 0; w < kProjWarps; ++w) s += wred[w][bb][j];
+      for (int w = 0; w < (NT / 32); ++w) s += wred[w][bb][j];
       cred[bb][j] = s;
     }
     __syncthreads();
@@ -250,14 +276,16 @@ project_kernel(ProjectArgs a) {
     const int share = (nout + CS - 1) / CS;
     {
       const uint32_t inc_addr = smem_u32(&incoming[0]);
-      for (int o = tid; o < nout; o += kProjThreads) {
+      for (int o = tid; o < nout; o += NT) {
         const int owner = o / share, ol = o - owner * share;
         st_dsmem_u32(mapa_shared(inc_addr + (rank * share + ol) * 4, owner),
                      __float_as_uint(cred[o / CPB][o % CPB]));
       }
     }
+    PJ_STAMP(5);
     cluster_sync_all();
-    for (int o = rank * share + tid; o < min(nout, (rank + 1) * share); o += kProjThreads) {
+    PJ_STAMP(6);
+    for (int o = rank * share + tid; o < min(nout, (rank + 1) * share); o += NT) {
       const int bb = o / CPB, j = o % CPB;
       const int cj = yb * CPB + j;
       const int ol = o - rank * share;
@@ -274,16 +302,33 @@ project_kernel(ProjectArgs a) {
         }
       }
     }
-    cluster_sync_all();
+    // (the incoming buffer is reused by the next pass; after the last pass no peer
+    // touches this CTA's shared memory any more: sync 1 ordered every DSMEM store)
+    if (b0 + kProjBT < a.B) cluster_sync_all();
+    PJ_STAMP(7);
   }
   pdl_launch_dependents();
 }
 
-template __global__ void project_kernel<float, 0>(ProjectArgs);
-template __global__ void project_kernel<float, 1>(ProjectArgs);
-template __global__ void project_kernel<float, 2>(ProjectArgs);
-template __global__ void project_kernel<__nv_bfloat16, 0>(ProjectArgs);
-template __global__ void project_kernel<__nv_bfloat16, 1>(ProjectArgs);
-template __global__ void project_kernel<__nv_bfloat16, 2>(ProjectArgs);
+}  // namespace sals
+extern "C" int sals_debug_proj_trace(unsigned long long* out) {
+#ifdef SALS_TC_TRACE
+  return (int)cudaMemcpyFromSymbol(out, sals::g_proj_trace, sizeof(sals::g_proj_trace));
+#else
+  (void)out;
+  return -1;
+#endif
+}
+namespace sals {
+
+#define SALS_PROJ_INST(T)                                              \
+  template __global__ void project_kernel<T, 0, 256>(ProjectArgs);     \
+  template __global__ void project_kernel<T, 1, 256>(ProjectArgs);     \
+  template __global__ void project_kernel<T, 2, 256>(ProjectArgs);     \
+  template __global__ void project_kernel<T, 0, 512>(ProjectArgs);     \
+  template __global__ void project_kernel<T, 1, 512>(ProjectArgs);     \
+  template __global__ void project_kernel<T, 2, 512>(ProjectArgs);
+SALS_PROJ_INST(float)
+SALS_PROJ_INST(__nv_bfloat16)
 
 }  // namespace sals
