@@ -776,10 +776,34 @@ sals_status sals_decode_profile(const sals_config* cfg, const void* U, const voi
 }
 
 // ------------------------------------------------------------ dense baseline
+// The TMA-streamed kernel (dense_tma.cu) where its shapes allow (bf16, d = 128,
+// n_kv a multiple of 8), else flash_decode_kernel; SALS_DENSE_LSU=1 forces the latter.
+static bool use_dense_tma(const sals_config* cfg) {
+  static const bool force_lsu = [] { const char* e = getenv("SALS_DENSE_LSU"); return e && e[0] == '1'; }();
+  return !force_lsu && dense_tma_supported(cfg->head_dim, cfg->num_kv_heads, cfg->num_q_heads / cfg->num_kv_heads,
+                                           cfg->dtype == SALS_BF16 ? 2 : 4);
+}
+static void plan_dense(const sals_config* cfg, int batch, int max_seq_len, int& nsplit, int& chunk) {
+  if (use_dense_tma(cfg)) {
+    int nsm = 0;
+    if (device_sm_count(&nsm) != cudaSuccess || nsm < 1) nsm = 148;
+    dense_tma_plan(batch, max_seq_len, cfg->head_dim, cfg->num_kv_heads, nsm, nsplit, chunk);
+  } else {
+    plan_flash(batch, cfg->num_kv_heads, max_seq_len, flash_tpw_unr(cfg), nsplit, chunk);
+  }
+}
+
+// threads of the dense append / query-RoPE kernels: one per rotation pair and per
+// 16-byte vector of a head row
+static int dense_rope_threads(const sals_config* cfg) {
+  const int half = cfg->head_dim / 2, nvec = cfg->head_dim * (int)esize(cfg) / 16;
+  return (int)align_up((size_t)std::max(half, nvec), 32);
+}
+
 size_t sals_dense_workspace_bytes(const sals_config* cfg, int32_t batch, int32_t max_seq_len) {
   if (validate(cfg) != SALS_OK || batch < 1 || max_seq_len < 1) return 0;
   int nsplit, chunk;
-  plan_flash(batch, cfg->num_kv_heads, max_seq_len, flash_tpw_unr(cfg), nsplit, chunk);
+  plan_dense(cfg, batch, max_seq_len, nsplit, chunk);
   return align_up((size_t)batch * cfg->num_q_heads * cfg->head_dim * 4, 256) +
          align_up((size_t)batch * cfg->num_q_heads * nsplit * (cfg->head_dim + 2) * 4, 256);
 }
@@ -795,8 +819,9 @@ sals_status sals_dense_append(const sals_config* cfg, const void* k_new, const v
   a.D = cfg->num_kv_heads * cfg->head_dim; a.head_dim = cfg->head_dim; a.n_kv = cfg->num_kv_heads;
   a.rope = make_rope(cfg);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (cfg->dtype == SALS_BF16) SALS_CUDA_TRY(launch(dense_append_kernel<__nv_bfloat16>, dim3(batch), dim3(256), 0, st, 0, a));
-  else SALS_CUDA_TRY(launch(dense_append_kernel<float>, dim3(batch), dim3(256), 0, st, 0, a));
+  const dim3 grid(cfg->num_kv_heads, batch), block(dense_rope_threads(cfg));
+  if (cfg->dtype == SALS_BF16) SALS_CUDA_TRY(launch(dense_append_kernel<__nv_bfloat16>, grid, block, 0, st, 0, a));
+  else SALS_CUDA_TRY(launch(dense_append_kernel<float>, grid, block, 0, st, 0, a));
   return SALS_OK;
 }
 
@@ -812,7 +837,8 @@ sals_status sals_dense_decode(const sals_config* cfg, const void* q, const void*
   if (ws_bytes < sals_dense_workspace_bytes(cfg, batch, max_seq_len))
     return fail(SALS_ERR_WORKSPACE_TOO_SMALL, "dense workspace too small");
   int nsplit, chunk;
-  plan_flash(batch, cfg->num_kv_heads, max_seq_len, flash_tpw_unr(cfg), nsplit, chunk);
+  plan_dense(cfg, batch, max_seq_len, nsplit, chunk);
+  const bool tma = use_dense_tma(cfg);
   char* ws = reinterpret_cast<char*>(workspace);
   float* qrope = reinterpret_cast<float*>(ws);
   float* part = reinterpret_cast<float*>(ws + align_up((size_t)batch * cfg->num_q_heads * cfg->head_dim * 4, 256));
@@ -820,12 +846,10 @@ sals_status sals_dense_decode(const sals_config* cfg, const void* q, const void*
   Plan p{};
   p.D = cfg->num_kv_heads * cfg->head_dim;
   p.G = cfg->num_q_heads / cfg->num_kv_heads;
-  p.proj_cs = 1;
-  p.proj_rows = std::min(p.D, 512);
-  // query RoPE via the projection kernel's second role (no projection columns)
-  ProjectArgs pa{};
-  pa.x = q; pa.x_stride = cfg->num_q_heads * cfg->head_dim; pa.B = batch; pa.n_q = cfg->num_q_heads;
-  pa.head_dim = cfg->head_dim; pa.qrope = qrope; pa.seq_len = d_seq_len; pa.rope = make_rope(cfg);
+  // query RoPE at s_b - 1 (fp32): one CTA per (query head, request)
+  DenseAppendArgs ra{};
+  ra.k_new = q; ra.head_dim = cfg->head_dim; ra.rope = make_rope(cfg);
+  const dim3 rgrid(cfg->num_q_heads, batch), rblock(dense_rope_threads(cfg));
   FlashArgs f{};
   f.qrope = qrope; f.kbase = k_cache; f.v_cache = v_cache; f.count = d_seq_len; f.cap = cap; f.D = p.D;
   f.k_stride = 0; f.n_q = cfg->num_q_heads; f.n_kv = cfg->num_kv_heads; f.nsplit = nsplit; f.chunk = chunk;
@@ -834,12 +858,19 @@ sals_status sals_dense_decode(const sals_config* cfg, const void* q, const void*
   m.partials = part; m.bh_stride = (int64_t)nsplit * (cfg->head_dim + 2); m.s_stride = cfg->head_dim + 2;
   m.nsplit = nsplit; m.n_q = cfg->num_q_heads; m.head_dim = cfg->head_dim; m.out = out; m.normalize = 1;
   if (cfg->dtype == SALS_BF16) {
-    SALS_CUDA_TRY(launch(project_kernel<__nv_bfloat16, 1, 256>, dim3(1, 1), dim3(256), 0, st, 1, pa));
-    s = launch_flash<__nv_bfloat16, true>(cfg, f, batch, st);
+    SALS_CUDA_TRY(launch(dense_qrope_kernel<__nv_bfloat16>, rgrid, rblock, 0, st, 0, ra, d_seq_len, qrope,
+                         (int)cfg->num_q_heads));
+    if (tma) {
+      SALS_CUDA_TRY(launch_dense_tma(f, batch, cfg->head_dim, p.G, st));
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+    } else {
+      s = launch_flash<__nv_bfloat16, true>(cfg, f, batch, st);
+    }
     if (s != SALS_OK) return s;
     return launch_merge<__nv_bfloat16>(cfg, m, batch, st);
   }
-  SALS_CUDA_TRY(launch(project_kernel<float, 1, 256>, dim3(1, 1), dim3(256), 0, st, 1, pa));
+  SALS_CUDA_TRY(launch(dense_qrope_kernel<float>, rgrid, rblock, 0, st, 0, ra, d_seq_len, qrope,
+                       (int)cfg->num_q_heads));
   s = launch_flash<float, true>(cfg, f, batch, st);
   if (s != SALS_OK) return s;
   return launch_merge<float>(cfg, m, batch, st);

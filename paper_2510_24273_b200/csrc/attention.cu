@@ -357,30 +357,57 @@ template __global__ void merge_kernel<__nv_bfloat16>(MergeArgs);
 // ---------------------------------------------------------------------------
 // Dense comparator cache write: k_cache[b, pos] = RoPE_pos(k_new[b]), v copy.
 // ---------------------------------------------------------------------------
+// One CTA per (KV head, request), one thread per rotation pair: every load of the
+// head is issued before any store (no store -> load ordering chain), the value row
+// is copied with 16-byte vectors.
 template <typename T>
 __global__ void dense_append_kernel(DenseAppendArgs a) {
-  const int b = blockIdx.x;
-  __shared__ float2 sth[128];   // per-lane indexed: keep the angle table out of param space
-  for (int i = threadIdx.x; i < a.head_dim / 2; i += blockDim.x) sth[i] = make_float2(a.rope.th_hi[i], a.rope.th_lo[i]);
-  __syncthreads();
+  const int g = blockIdx.x, b = blockIdx.y, p = threadIdx.x;
+  const int half = a.head_dim / 2;
+  const float2 th = p < half ? make_float2(a.rope.th_hi[p], a.rope.th_lo[p]) : make_float2(0.f, 0.f);
   pdl_wait();
   const int64_t pos = a.pos[b];
-  const T* k = reinterpret_cast<const T*>(a.k_new) + (size_t)b * a.D;
-  const T* v = reinterpret_cast<const T*>(a.v_new) + (size_t)b * a.D;
-  T* kc = reinterpret_cast<T*>(a.k_cache) + ((size_t)b * a.cap + pos) * a.D;
-  T* vc = reinterpret_cast<T*>(a.v_cache) + ((size_t)b * a.cap + pos) * a.D;
-  const int half = a.head_dim / 2;
-  for (int t = threadIdx.x; t < a.n_kv * half; t += blockDim.x) {
-    const int g = t / half, p = t % half;
+  const T* __restrict__ k = reinterpret_cast<const T*>(a.k_new) + (size_t)b * a.D + (size_t)g * a.head_dim;
+  const T* __restrict__ v = reinterpret_cast<const T*>(a.v_new) + (size_t)b * a.D + (size_t)g * a.head_dim;
+  T* __restrict__ kc = reinterpret_cast<T*>(a.k_cache) + ((size_t)b * a.cap + pos) * a.D + (size_t)g * a.head_dim;
+  T* __restrict__ vc = reinterpret_cast<T*>(a.v_cache) + ((size_t)b * a.cap + pos) * a.D + (size_t)g * a.head_dim;
+  constexpr int EPV = 16 / sizeof(T);
+  const int nvec = a.head_dim / EPV;
+  uint4 vv = make_uint4(0, 0, 0, 0);
+  if (p < nvec) vv = *reinterpret_cast<const uint4*>(v + p * EPV);
+  if (p < half) {
     int lo, hi; rope_pair(p, half, a.rope.style, lo, hi);
-    float c, s; rope_cs_fast(sth[p].x, sth[p].y, (int)pos, c, s);
-    const float xl = Elem<T>::to_f(k[g * a.head_dim + lo]), xh = Elem<T>::to_f(k[g * a.head_dim + hi]);
-    kc[g * a.head_dim + lo] = Elem<T>::from_f(xl * c - xh * s);
-    kc[g * a.head_dim + hi] = Elem<T>::from_f(xl * s + xh * c);
+    const float xl = Elem<T>::to_f(k[lo]), xh = Elem<T>::to_f(k[hi]);
+    float c, sn; rope_cs_fast(th.x, th.y, (int)pos, c, sn);
+    kc[lo] = Elem<T>::from_f(xl * c - xh * sn);
+    kc[hi] = Elem<T>::from_f(xl * sn + xh * c);
   }
-  for (int i = threadIdx.x; i < a.D; i += blockDim.x) vc[i] = v[i];
+  if (p < nvec) *reinterpret_cast<uint4*>(vc + p * EPV) = vv;
   pdl_launch_dependents();
 }
+
+// Query RoPE of the dense comparator: qrope[b, h] = RoPE_{s_b - 1}(q[b, h]) (fp32),
+// one CTA per (query head, request), one thread per rotation pair.
+template <typename T>
+__global__ void dense_qrope_kernel(DenseAppendArgs a, const int* seq_len, float* qrope, int n_q) {
+  const int h = blockIdx.x, b = blockIdx.y, p = threadIdx.x;
+  const int half = a.head_dim / 2;
+  const float2 th = p < half ? make_float2(a.rope.th_hi[p], a.rope.th_lo[p]) : make_float2(0.f, 0.f);
+  pdl_wait();
+  if (p < half) {
+    const int pos = seq_len[b] - 1;
+    const T* q = reinterpret_cast<const T*>(a.k_new) + ((size_t)b * n_q + h) * a.head_dim;
+    float* o = qrope + ((size_t)b * n_q + h) * a.head_dim;
+    int lo, hi; rope_pair(p, half, a.rope.style, lo, hi);
+    const float xl = Elem<T>::to_f(q[lo]), xh = Elem<T>::to_f(q[hi]);
+    float c, sn; rope_cs_fast(th.x, th.y, pos, c, sn);
+    o[lo] = xl * c - xh * sn;
+    o[hi] = xl * sn + xh * c;
+  }
+  pdl_launch_dependents();
+}
+template __global__ void dense_qrope_kernel<float>(DenseAppendArgs, const int*, float*, int);
+template __global__ void dense_qrope_kernel<__nv_bfloat16>(DenseAppendArgs, const int*, float*, int);
 template __global__ void dense_append_kernel<float>(DenseAppendArgs);
 template __global__ void dense_append_kernel<__nv_bfloat16>(DenseAppendArgs);
 

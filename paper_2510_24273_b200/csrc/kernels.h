@@ -134,10 +134,15 @@ template <typename T, int LG, int CPL> __global__ void latent_score_kernel(Score
 // Single-CTA histogram-assisted top-k for <= 8192 entries per request (topk_cta.cu).
 cudaError_t launch_topk_cta(const TopkArgs& a, int batch, int max_entries, cudaStream_t st);
 cudaError_t launch_score_tma(const ScoreArgs& a, int batch, int max_len, cudaStream_t st, int nsm);
+// TMA-streamed dense comparator (dense_tma.cu); cudaErrorNotSupported outside its shapes.
+bool dense_tma_supported(int head_dim, int n_kv, int G, int dtype_bytes);
+void dense_tma_plan(int batch, int max_len, int head_dim, int n_kv, int nsm, int& nsplit, int& chunk);
+cudaError_t launch_dense_tma(const FlashArgs& a, int batch, int head_dim, int G, cudaStream_t st);
 template <int NT> __global__ void topk_hist_kernel(TopkArgs a);
 template <typename T> __global__ void recon_rope_simt_kernel(ReconArgs a);
 template <typename T, int DH, int G, bool DENSE> __global__ void flash_decode_kernel(FlashArgs a);
 template <typename T> __global__ void merge_kernel(MergeArgs a);
 template <typename T> __global__ void dense_append_kernel(DenseAppendArgs a);
+template <typename T> __global__ void dense_qrope_kernel(DenseAppendArgs a, const int* seq_len, float* qrope, int n_q);
 
 }  // namespace sals

@@ -413,8 +413,9 @@ cudaError_t launch_g(const CUtensorMap& map, const TcArgs& a, int batch, cudaStr
 
 }  // namespace
 
-cudaError_t launch_recon_attn_tc2(const CUtensorMap& map, const CUtensorMap& ml, const CUtensorMap& mv,
-                                  const CUtensorMap& mvh, const TcArgs& a, int batch, cudaStream_t st);
+cudaError_t launch_recon_attn_tc2(const CUtensorMap& map, const CUtensorMap& map_u128, const CUtensorMap& ml,
+                                  const CUtensorMap& mv, const CUtensorMap& mvh, const TcArgs& a, int batch,
+                                  cudaStream_t st);
 
 bool tc_supported(int head_dim, int D, int rank, int G) {
   return (head_dim == 64 || head_dim == 128 || head_dim == 256) && D % kBN == 0 && rank % kBK == 0 &&
@@ -478,7 +479,16 @@ sals_status launch_recon_attn_tc(const TcArgs& a, int batch, cudaStream_t st) {
         return SALS_ERR_CUDA;
       }
     }
-    e = launch_recon_attn_tc2(map, ml, mv, mvh, a, batch, st);
+    // (cta_group::2 variant) U boxes of 128 columns: one half of the pair's 256 per CTA
+    CUtensorMap mu2;
+    cuuint32_t box2[2] = {kBK, kBN / 2};
+    if (g_encode(&mu2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a.U), dims, strides, box2, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      g_tc_err = "cuTensorMapEncodeTiled failed for the 128-column U map";
+      return SALS_ERR_CUDA;
+    }
+    e = launch_recon_attn_tc2(map, mu2, ml, mv, mvh, a, batch, st);
     if (e != cudaSuccess) { g_tc_err = cudaGetErrorString(e); return SALS_ERR_CUDA; }
     return SALS_OK;
   }

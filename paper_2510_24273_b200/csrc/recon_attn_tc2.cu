@@ -30,17 +30,18 @@ namespace sals {
 namespace tc2 {
 
 constexpr int kRows = 128, kBK = 64, kBN = 256, kStages = 3, kDH = 128;
+constexpr int kStages2 = 4;   // cta_group::2 (MHA): 16 KB A + 16 KB U half per stage
 constexpr int kThreads = 512;
 constexpr int kABytes = kRows * kBK * 2;   // 16 KB
 constexpr int kBBytes = kBN * kBK * 2;     // 32 KB
 constexpr int kVBytes = kRows * kBN * 2;   // 64 KB
 constexpr int kPS = kRows + 4;             // sP row stride (floats): the two KV-head halves of a warp hit different banks
 
-__host__ __device__ constexpr int smem_bytes(int G);
+__host__ __device__ constexpr int smem_bytes(int G, int CG = 1);
 static_assert(1024 + 3 * (128 * 64 * 2 + 256 * 64 * 2) + 128 * 256 * 2 + 8 * 64 * 8 + 16 * 128 * 4 + 8 * (128 + 4) * 4 + 1024 <=
                   232448, "G = 4 shared memory over the 227 KB limit");
-__host__ __device__ constexpr int smem_bytes(int G) {
-  return 1024 + kStages * (kABytes + kBBytes) + kVBytes + 2 * G * 64 * 8 /*sQ*/ + 2 * 2 * G * kRows * 4 /*sL*/ +
+__host__ __device__ constexpr int smem_bytes(int G, int CG) {
+  return 1024 + (CG == 2 ? kStages2 * (kABytes + kBBytes / 2) : kStages * (kABytes + kBBytes)) + kVBytes + 2 * G * 64 * 8 /*sQ*/ + 2 * 2 * G * kRows * 4 /*sL*/ +
          (2 * G * kPS * 4 > 4096 ? 2 * G * kPS * 4 : 4096) /*sP*/ + 1024 /*misc: sRed, sAl, sIdxV, barriers, TMEM slot (< 1 KB)*/;
 }
 
@@ -117,6 +118,45 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64
       "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accum)
       : "memory");
 }
+// ---- cta_group::2 (a CTA pair computes M = 256 rows: each CTA its 128 token rows and
+// half of the 256 U columns; the even CTA issues the MMAs into both CTAs' TMEM)
+constexpr uint32_t kIdesc2 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kBN >> 3) << 17) |
+                             ((uint32_t)(256 >> 4) << 24);
+__device__ __forceinline__ void mma_bf16_cg2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc2), "r"(accum)
+      : "memory");
+}
+// arrive on the barrier at this offset in both CTAs of the pair
+__device__ __forceinline__ void mma_commit_cg2(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"((uint16_t)3)
+               : "memory");
+}
+// shared::cluster address of this CTA's `p` in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_rank(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -193,6 +233,7 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
 
 struct KArgs {
   TcArgs a;
+  int axis;   // (CG = 2) the pair: 1 = consecutive chunks, 3 = consecutive requests
 };
 
 // Split merge fused into the kernel: every chunk CTA of (request b, column block
@@ -206,13 +247,13 @@ __device__ __forceinline__ void merge_if_last(const TcArgs& a, int b, int nb, in
   __syncthreads();
   if (tid == 0) {
     const unsigned old = atomicAdd(&a.counters[(size_t)b * gridDim.y + nb], 1u);   // after the partials' fences
-    s_last = old == gridDim.x - 1;
+    s_last = old == (unsigned)a.ntiles - 1;
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
   if (tid == 0) a.counters[(size_t)b * gridDim.y + nb] = 0;   // every chunk CTA has arrived: re-arm
-  const int ns = gridDim.x;
+  const int ns = a.ntiles;   // chunks per request
   // the NQH heads' partials [NQH][ns][d+2] are one contiguous block: stage it in
   // shared memory with a single round of independent 8-byte loads, then merge
   // (log-sum-exp, split order) from shared memory
@@ -257,12 +298,28 @@ __device__ unsigned long long g_trace[128];
 #else
 #define TSTAMP(slot) do {} while (0)
 #endif
+#ifdef SALS_TC_CTATIME
+// per-CTA globaltimer stamps (ns): [cta][0 start, 1 after the PDL wait, 2 last MMA issued, 3 end]
+__device__ unsigned long long g_ctatime[1024][4];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define CTIME(slot)                                                                                         \
+  do {                                                                                                      \
+    const unsigned cid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);                    \
+    if (cid < 1024) g_ctatime[cid][(slot)] = gtimer();                                                      \
+  } while (0)
+#else
+#define CTIME(slot) do {} while (0)
+#endif
 
 // VBH: 16 = dtype (bf16) value rows; 4 / 2 = quantised value rows (DESIGN R15):
 // per KV head 128*VB/8 code bytes then 4 (bf16 scale, bf16 zero) pairs;
 // 40 / 20 = the same with the 8-bit recent window (a compile-time variant so the
 // kernels without the window carry none of its code).
-template <int G, int STYLE, int VBH>
+template <int G, int STYLE, int VBH, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
 recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_constant__ CUtensorMap tmap_lat,
                       const __grid_constant__ CUtensorMap tmap_v, const __grid_constant__ CUtensorMap tmap_vh,
@@ -277,6 +334,12 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
   // times): c3 / c4 31.9 -> 28.0 us, c2 22.8 -> 23.8 us (the 16-byte V copies compete
   // with the A operand's cp.async), hence G >= 2 only.
   constexpr bool TPV = VB == 16 && G >= 2;
+  // CG = 2: MHA with dtype values only (every tcgen05 op of a kernel uses one cta_group,
+  // and the GQA P V runs per CTA)
+  constexpr bool C2 = CG == 2;
+  static_assert(!C2 || (G == 1 && VBH == 16), "cta_group::2 variant: MHA, bf16 values");
+  constexpr int ST = C2 ? kStages2 : kStages;             // operand ring depth
+  constexpr int kBHalf = C2 ? kBBytes / 2 : kBBytes;       // U bytes per stage in this CTA
   constexpr int kVHead = VB == 16 ? kDH * 2 : kDH * VB / 8 + (kDH / 32) * 4;   // value bytes per head-token
   constexpr int kVRow = 2 * kVHead;                                           // bytes of a V tile row (2 heads)
   constexpr int kVRowH = 2 * 144;   // (quantised) 8-bit recent-window row of the 2 heads (DESIGN R15)
@@ -288,8 +351,8 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
   // address space (an integer round trip would turn every access into a generic load)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
-  uint8_t* sB = sA + kStages * kABytes;
-  uint8_t* sV = sB + kStages * kBBytes;
+  uint8_t* sB = sA + ST * kABytes;
+  uint8_t* sV = sB + ST * kBHalf;
   float2* sQ = reinterpret_cast<float2*>(sV + kVBytes);          // [NQH][64] (q_lo, q_hi) per pair
   float* sL = reinterpret_cast<float*>(sQ + NQH * 64);           // [2 halves][NQH][128] partial logits
   float* sP = sL + 2 * NQH * kRows;                              // [NQH][kPS] probabilities
@@ -298,29 +361,35 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
   int* sIdxV = reinterpret_cast<int*>(sAl + NQH);                // [128] global rows of the V tile
   uint64_t* bars = reinterpret_cast<uint64_t*>(sIdxV + kRows);
   uint64_t* full = bars;                 // [stages]
-  uint64_t* empty = bars + kStages;      // [stages]
-  uint64_t* tfull = bars + 2 * kStages;  // [2]
+  uint64_t* empty = bars + ST;           // [stages]
+  uint64_t* tfull = bars + 2 * ST;       // [2]
   uint64_t* tempty = tfull + 2;          // [2]
   uint64_t* vfull = tempty + 2;
   uint64_t* vempty = vfull + 1;
   uint64_t* pready = vempty + 1;          // (TPV) [2] P of the tile written (epilogue -> MMA warp)
   uint64_t* pvfull = pready + 2;          // (TPV) [2] O_tile in TMEM (tcgen05.commit -> epilogue)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pvfull + 2);
+  uint64_t* pfull = pvfull + 2;           // (C2, even CTA) [stages] both CTAs' stage landed (2 relays)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pfull + ST);
   int* s_thp = reinterpret_cast<int*>(tmem_slot + 1);   // first tile token read from the 8-bit recent window
   uint8_t* sVh = sV + kRows * kVRow;                      // (quantised) 8-bit rows of the recent window
   static_assert(VB == 16 || kRows * kVRow + 32 * 1280 <= kVBytes, "recent-window staging exceeds the V tile");
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int chunk = blockIdx.x, nb = blockIdx.y, b = blockIdx.z;
+  // (C2, pair of requests: the cluster pairs along x, which a cta_group::2 launch needs,
+  // so x = 2 chunk + (b & 1), z = b / 2)
+  const bool zpair = C2 && ka.axis == 3;
+  const int chunk = zpair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x, nb = blockIdx.y;
+  const int b = zpair ? (int)(2 * blockIdx.z + (blockIdx.x & 1)) : (int)blockIdx.z;
   const int n0 = nb * kBN;
+  if (tid == 0) CTIME(0);
 
   // Prologue before griddepcontrol.wait (overlaps the top-k kernel, which triggers
   // its dependents early): barriers, TMEM allocation and the rotated queries
   // (q^R comes from the query projection, which completed before the top-k's
   // upstream did).  Only the selection (sel / count) is read after the wait.
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 128 + 1); mbar_init(&empty[s], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8); }
+    for (int s = 0; s < ST; ++s) { mbar_init(&full[s], 128 + 1); mbar_init(&empty[s], 1); mbar_init(&pfull[s], 2); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], C2 ? 16 : 8); }
     mbar_init(vfull, TPV ? 256 : 1);   // TPV: the 256 epilogue threads' cp.async; else one expect_tx
     mbar_init(vempty, 1);
     for (int i = 0; i < 2; ++i) { mbar_init(&pready[i], 1); mbar_init(&pvfull[i], 1); }
@@ -330,9 +399,15 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
     for (int i = tid; i < 4096 / 16; i += kThreads) reinterpret_cast<uint4*>(sP)[i] = make_uint4(0, 0, 0, 0);
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(512));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (C2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(512));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(512));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   if (warp >= 8) {   // rotated, scaled queries: sQ4[qh][p/2] = (q_lo(p), q_lo(p+1), q_hi(p), q_hi(p+1))
     float4* sQ4 = reinterpret_cast<float4*>(sQ);
@@ -348,19 +423,33 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
   if (tid == 0) TSTAMP(80);
   pdl_wait();
   if (tid == 0) TSTAMP(82);
+  if (tid == 0) CTIME(1);
   const int cnt = a.count[b];
   const int ntiles_b = (cnt + kRows - 1) / kRows;
   const int t_begin = chunk * a.tiles_per_cta;
   const int t_end = min(ntiles_b, t_begin + a.tiles_per_cta);
   const int ntile = max(0, t_end - t_begin);
   const int* selb = a.sel + (size_t)b * a.k_stride;
+  // (C2) both CTAs of the pair run the same number of pair steps: the larger tile count;
+  // a CTA past its own tiles contributes zero rows and skips their epilogue
+  const uint32_t crank = C2 ? cluster_ctarank() : 0u;
+  int ntile_pair = ntile;
+  if constexpr (C2) {
+    const int pchunk = ka.axis == 1 ? (chunk ^ 1) : chunk, pb = ka.axis == 3 ? (b ^ 1) : b;
+    const int pcnt = a.count[pb];
+    const int pt0 = pchunk * a.tiles_per_cta;
+    const int pt1 = min((pcnt + kRows - 1) / kRows, pt0 + a.tiles_per_cta);
+    ntile_pair = max(ntile, pt1 - pt0);
+  }
 
-  if (ntile == 0) {   // no selected tokens for this chunk: empty partials (m = -inf, l = 0, o = 0)
+  if (ntile_pair == 0) {   // no selected tokens for this chunk: empty partials (m = -inf, l = 0, o = 0)
     tc_fence_before();
     __syncthreads();
+    if constexpr (C2) cluster_sync_all();
     if (warp == 1) {
       tc_fence_after();
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "r"(512));
+      if constexpr (C2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "r"(512));
+      else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "r"(512));
     }
     for (int i = tid; i < NQH * (kDH + 2); i += kThreads) {
       const int qh = i / (kDH + 2), j = i - qh * (kDH + 2);
@@ -374,6 +463,7 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
 
   tc_fence_before();
   __syncthreads();
+  if constexpr (C2) cluster_sync_all();   // the peer's barriers / TMEM exist before any remote use
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int nk = a.r / kBK;
@@ -381,16 +471,59 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
   if (warp == 0) {
     // ================= U (B operand) producer: one TMA per K chunk =================
     if (lane == 0) {
+      // (C2: this CTA's half, the U columns n0 + 128 crank .. +128, from a 128-row box map)
       int u = 0;
-      for (int it = 0; it < ntile; ++it)
+      for (int it = 0; it < ntile_pair; ++it)
         for (int kc = 0; kc < nk; ++kc, ++u) {
-          const int s = u % kStages;
-          if (u >= kStages) mbar_wait(&empty[s], ((u / kStages) - 1) & 1);
+          const int s = u % ST;
+          if (u >= ST) mbar_wait(&empty[s], ((u / ST) - 1) & 1);
 #ifdef SALS_EXP_NO_U   // experiment (trace builds only): U fetched for the first stages only
-          if (u >= kStages) { mbar_arrive(&full[s]); continue; }
+          if (u >= ST) { mbar_arrive(&full[s]); continue; }
 #endif
-          mbar_arrive_expect_tx(&full[s], kBBytes);
-          tma_load_2d(smem_u32(sB + s * kBBytes), &tmap_u, kc * kBK, n0, &full[s]);
+          mbar_arrive_expect_tx(&full[s], kBHalf);
+          tma_load_2d(smem_u32(sB + s * kBHalf), &tmap_u, kc * kBK, n0 + (int)crank * (kBN / 2), &full[s]);
+        }
+      if constexpr (C2) {   // the even CTA's last commits (multicast) have reached this CTA's slots
+        for (int v = max(0, u - ST); v < u; ++v) mbar_wait(&empty[v % ST], (v / ST) & 1);
+      }
+    }
+  } else if (C2 && warp == 1) {
+    // ================= MMA issuer (cta_group::2): the even CTA, M = 256 over the pair =================
+    if (lane == 0 && crank == 0) {
+      int u = 0;
+      for (int it = 0; it < ntile_pair; ++it) {
+        const int buf = it & 1;
+        if (it >= 2) mbar_wait_cluster(&tempty[buf], ((it >> 1) - 1) & 1);   // both CTAs' epilogues
+        TSTAMP(0 + it);
+        tc_fence_after();
+        const uint32_t acc = tmem + buf * kBN;
+        for (int kc = 0; kc < nk; ++kc, ++u) {
+          const int s = u % ST;
+          mbar_wait_cluster(&pfull[s], (u / ST) & 1);
+          if (kc == 0) TSTAMP(88 + it);
+          tc_fence_after();
+          const uint32_t ab = smem_u32(sA + s * kABytes), bb = smem_u32(sB + s * kBHalf);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            mma_bf16_cg2(acc, sw128_desc(ab + k * 32), sw128_desc(bb + k * 32), (kc | k) ? 1u : 0u);
+          mma_commit_cg2(&empty[s]);
+        }
+        mma_commit_cg2(&tfull[buf]);
+        TSTAMP(8 + it);
+      }
+      CTIME(2);
+      pdl_launch_dependents();
+    }
+  } else if (C2 && warp == 3) {
+    // ================= (C2) relay: this CTA's stage landed -> the even CTA's pfull =================
+    if (lane == 0) {
+      int u = 0;
+      for (int it = 0; it < ntile_pair; ++it)
+        for (int kc = 0; kc < nk; ++kc, ++u) {
+          const int s = u % ST;
+          mbar_wait(&full[s], (u / ST) & 1);
+          fence_proxy_async();   // the cp.async-written A rows -> the tensor core's proxy
+          mbar_arrive_remote(mapa_rank(&pfull[s], 0));
         }
     }
   } else if (warp == 1) {
@@ -434,14 +567,14 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
         tc_fence_after();
         const uint32_t acc = tmem + buf * kBN;
         for (int kc = 0; kc < nk; ++kc, ++u) {
-          const int s = u % kStages;
+          const int s = u % ST;
           if constexpr (TPV) {
-            while (!mbar_test(&full[s], (u / kStages) & 1)) issue_pv(false);
+            while (!mbar_test(&full[s], (u / ST) & 1)) issue_pv(false);
           }
-          mbar_wait(&full[s], (u / kStages) & 1);
+          mbar_wait(&full[s], (u / ST) & 1);
           tc_fence_after();
           fence_proxy_async();
-          const uint32_t ab = smem_u32(sA + s * kABytes), bb = smem_u32(sB + s * kBBytes);
+          const uint32_t ab = smem_u32(sA + s * kABytes), bb = smem_u32(sB + s * kBHalf);
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k)
             mma_bf16(acc, sw128_desc(ab + k * 32), sw128_desc(bb + k * 32), (kc | k) ? 1u : 0u);
@@ -452,6 +585,7 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
         while (issue_pv(false)) {}
       }
       if constexpr (TPV) { while (pv < ntile) issue_pv(true); }
+      CTIME(2);
       // all MMAs issued: the next kernel may launch and run its pre-wait prologue
       // (the projection stages U, a weight) while this CTA's last epilogue runs
       pdl_launch_dependents();
@@ -543,11 +677,11 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
     };
     int rows[8], rows_nx[8];
     load_rows(t_begin, rows);
-    for (int it = 0; it < ntile; ++it) {
-      if (it + 1 < ntile) load_rows(t_begin + it + 1, rows_nx);
+    for (int it = 0; it < ntile_pair; ++it) {   // (C2: past this CTA's tiles no row is valid -> zero fill)
+      if (it + 1 < ntile_pair) load_rows(t_begin + it + 1, rows_nx);
       for (int kc = 0; kc < nk; ++kc, ++u) {
-        const int s = u % kStages;
-        if (u >= kStages) mbar_wait(&empty[s], ((u / kStages) - 1) & 1);
+        const int s = u % ST;
+        if (u >= ST) mbar_wait(&empty[s], ((u / ST) - 1) & 1);
         const uint32_t base = smem_u32(sA + s * kABytes);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -586,8 +720,16 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
     // the token row of tile it+1 is loaded during tile it (its L2 round trip would
     // otherwise sit in front of the first RoPE angle of every tile)
     int row_nx = m < min(kRows, cnt - t_begin * kRows) ? selb[t_begin * kRows + m] : -1;
-    for (int it = 0; it < ntile; ++it) {
+    for (int it = 0; it < ntile_pair; ++it) {
       const int tile = t_begin + it, buf = it & 1;
+      if (C2 && it >= ntile) {   // the partner's tile: release the accumulator, nothing to compute
+        mbar_wait(&tfull[buf], (it >> 1) & 1);
+        tc_fence_after();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(mapa_rank(&tempty[buf], 0));
+        continue;
+      }
       const int nv = min(kRows, cnt - tile * kRows);
       const int row = row_nx;
       if (it + 1 < ntile) row_nx = m < min(kRows, cnt - (tile + 1) * kRows) ? selb[(tile + 1) * kRows + m] : -1;
@@ -678,7 +820,10 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
       if constexpr (!TPV) {   // (TPV: the buffer also receives the tile's P V; released after it)
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[buf]);     // this warp is done with the accumulator
+        if (lane == 0) {                               // this warp is done with the accumulator
+          if constexpr (C2) mbar_arrive_remote(mapa_rank(&tempty[buf], 0));
+          else mbar_arrive(&tempty[buf]);
+        }
       }
 #pragma unroll
       for (int j = 0; j < 2; ++j)
@@ -874,7 +1019,7 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const int h = nb * NQH + hf * G + g;
-      if (a.direct_out && gridDim.x == 1) {
+      if (a.direct_out && a.ntiles == 1) {
         __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(a.direct_out) + ((size_t)b * a.n_q + h) * kDH;
         y[n] = __float2bfloat16_rn(l_run[g] > 0.f ? o[g] / l_run[g] : 0.f);
       } else {
@@ -883,42 +1028,73 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
         if (n == 0) { dst[0] = m_run[g]; dst[1] = l_run[g]; }
       }
     }
-    if (a.counters && gridDim.x > 1) __threadfence();
+    if (a.counters && a.ntiles > 1) __threadfence();
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (C2) cluster_sync_all();   // every remote arrive / MMA of the pair has landed
   if (tid == 0) TSTAMP(81);
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    if constexpr (C2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
-  if (a.counters && gridDim.x > 1) merge_if_last<NQH>(a, b, nb, tid, reinterpret_cast<float*>(smem));
+  if (tid == 0) CTIME(3);
+  if (a.counters && a.ntiles > 1) merge_if_last<NQH>(a, b, nb, tid, reinterpret_cast<float*>(smem));
   pdl_launch_dependents();
 }
 
-template <int G, int STYLE, int VBH>
+template <int G, int STYLE, int VBH, int CG = 1>
 cudaError_t launch_t(const CUtensorMap& map, const CUtensorMap& map_lat, const CUtensorMap& map_v,
-                     const CUtensorMap& map_vh, const TcArgs& a, int batch, cudaStream_t st) {
-  auto kern = recon_attn_tc2_kernel<G, STYLE, VBH>;
+                     const CUtensorMap& map_vh, const TcArgs& a, int batch, cudaStream_t st, int axis = 0) {
+  auto kern = recon_attn_tc2_kernel<G, STYLE, VBH, CG>;
   static DeviceOnce once;
-  cudaError_t e = once.run([&] { return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(G)); });
+  cudaError_t e = once.run([&] {
+    cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(G, CG));
+    return r;
+  });
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(a.ntiles, a.D / kBN, batch);
+  cfg.gridDim = (CG == 2 && axis == 3) ? dim3(2 * a.ntiles, a.D / kBN, batch / 2) : dim3(a.ntiles, a.D / kBN, batch);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem_bytes(G);
+  cfg.dynamicSmemBytes = smem_bytes(G, CG);
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = CG == 2 ? 2 : 1;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
-  KArgs ka{a};
+  cfg.numAttrs = CG == 2 ? 2 : 1;
+  KArgs ka{a, axis};
   return cudaLaunchKernelEx(&cfg, kern, map, map_lat, map_v, map_vh, ka);
 }
 
+// MHA with bf16 values on a CTA pair (cta_group::2, M = 256: each U tile is read once per
+// pair instead of once per CTA) when the grid pairs up: consecutive chunks, else requests.
+// Opt-in (SALS_TC2_CG=2): parity-green but measured slower than the one-CTA kernel at c2
+// (profiles/r2/experiments).
+int tc2_pair_axis(const TcArgs& a, int batch) {
+  static const bool on = [] { const char* e = getenv("SALS_TC2_CG"); return e && e[0] == '2'; }();
+  if (!on || a.G != 1 || a.v_bits != 0) return 0;
+  if (a.ntiles % 2 == 0) return 1;
+  if (batch % 2 == 0) return 3;
+  return 0;
+}
+
 }  // namespace tc2
+
+extern "C" int sals_debug_tc_ctatime(unsigned long long* host_out) {
+#ifdef SALS_TC_CTATIME
+  return (int)cudaMemcpyFromSymbol(host_out, tc2::g_ctatime, sizeof(tc2::g_ctatime));
+#else
+  (void)host_out;
+  return -1;
+#endif
+}
 
 extern "C" int sals_debug_tc_trace(unsigned long long* host_out) {
 #ifdef SALS_TC_TRACE
@@ -938,9 +1114,15 @@ bool tc2_supported(int head_dim, int D, int rank, int G) {
   return head_dim == 128 && D % tc2::kBN == 0 && rank % tc2::kBK == 0 && (G == 1 || G == 2 || G == 4);
 }
 
-cudaError_t launch_recon_attn_tc2(const CUtensorMap& map, const CUtensorMap& ml, const CUtensorMap& mv,
-                                  const CUtensorMap& mvh, const TcArgs& a, int batch, cudaStream_t st) {
+cudaError_t launch_recon_attn_tc2(const CUtensorMap& map, const CUtensorMap& map_u128, const CUtensorMap& ml,
+                                  const CUtensorMap& mv, const CUtensorMap& mvh, const TcArgs& a, int batch,
+                                  cudaStream_t st) {
   const int style = a.rope.style;
+  const int axis = tc2::tc2_pair_axis(a, batch);
+  if (axis) {
+    return style ? tc2::launch_t<1, 1, 16, 2>(map_u128, ml, mv, mvh, a, batch, st, axis)
+                 : tc2::launch_t<1, 0, 16, 2>(map_u128, ml, mv, mvh, a, batch, st, axis);
+  }
 #define SALS_TC2_VB(VB)                                                                                         \
   switch (a.G) {                                                                                                \
     case 1: return style ? tc2::launch_t<1, 1, VB>(map, ml, mv, mvh, a, batch, st) : tc2::launch_t<1, 0, VB>(map, ml, mv, mvh, a, batch, st); \

@@ -182,6 +182,15 @@ def test_c5_grid_points(B, n):
     print(B, n, stats)
 
 
+@pytest.mark.parametrize("B,seqs", [(4, [4096, 100, 2000, 1]), (8, [4096, 4000, 1, 1, 700, 4096, 129, 3000])])
+def test_ragged_requests_c2_heads(B, seqs):
+    """MHA at c2's head shape (D = 4096, one chunk per request in the fused kernel)
+    with very different selection counts per request (1 to 4 tiles, one-token
+    requests), every output element against the oracle."""
+    sh = _shape("c2")
+    H.full_check(sh, B, seqs, seed=61 + B)
+
+
 def test_full_size_ragged_c3():
     sh = _shape("c3")
     H.full_check(sh, 4, [32768, 17, 4096, 30001], seed=21)
@@ -215,6 +224,37 @@ def test_dense_decode(dtype, G):
     torch.cuda.synchronize()
     y = O.dense_decode(oc, H.widen(qt), H.widen(kc), H.widen(vc), seq_lens)
     H.check_output(H.widen(out), y, dtype)
+
+
+@pytest.mark.parametrize("nkv,G,B,cap,lens", [
+    (8, 4, 4, 3000, [3000, 1, 1777, 9]),        # D = 1024 (c3 / c4 heads): TMA kernel, 8 tokens per stage
+    (8, 2, 3, 2051, [2051, 2, 1000]),
+    (8, 8, 2, 999, [999, 31]),
+    (8, 1, 2, 40000, [40000, 33333]),           # long rows: many stages per CTA
+    (32, 1, 3, 1025, [1025, 1, 513]),           # D = 4096 (c2 heads): flash_decode_kernel
+])
+def test_dense_decode_full_shapes(nkv, G, B, cap, lens):
+    """The dense comparator at the paper's head shapes (dense_tma.cu for 8 KV heads,
+    flash_decode_kernel otherwise) vs the oracle's dense decode, ragged lengths
+    (partial stages, one-token requests, empty splits)."""
+    from paper_2510_24273_b200 import sals
+    d = 128
+    sh = dict(num_q_heads=nkv * G, num_kv_heads=nkv, head_dim=d, rank=64, score_rank=32, top_k=64, rope_base=1e4)
+    cfg = sals.make_config(**sh)
+    oc = O.Config(num_q_heads=nkv * G, num_kv_heads=nkv, head_dim=d, rank=64, score_rank=32, top_k=64, rope_base=1e4)
+    rng = np.random.default_rng(50 + nkv + G)
+    seq_lens = np.array(lens, dtype=np.int32)
+    D = nkv * d
+    kc = torch.from_numpy(rng.standard_normal((B, cap, D)).astype(np.float32)).cuda().bfloat16()
+    vc = torch.from_numpy(rng.standard_normal((B, cap, D)).astype(np.float32)).cuda().bfloat16()
+    qt = torch.from_numpy((2.0 * rng.standard_normal((B, nkv * G * d))).astype(np.float32)).cuda().bfloat16()
+    seq = torch.from_numpy(seq_lens).cuda()
+    ws = sals.alloc_workspace(sals.sals_dense_workspace_bytes(cfg, B, cap), "cuda")
+    out = torch.empty(B, nkv * G * d, dtype=torch.bfloat16, device="cuda")
+    sals.sals_dense_decode(cfg, qt, kc, vc, seq, cap, out, ws)
+    torch.cuda.synchronize()
+    y = O.dense_decode(oc, H.widen(qt), H.widen(kc), H.widen(vc), seq_lens)
+    H.check_output(H.widen(out), y, "bf16")
 
 
 def test_dense_append_positions():
