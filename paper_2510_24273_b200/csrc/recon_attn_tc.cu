@@ -369,13 +369,62 @@ thread_local std::string g_tc_err;
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_encode_once;
 
+PFN_cuTensorMapEncodeTiled_v12000 g_encode_drv = nullptr;
+
+// cuTensorMapEncodeTiled is a pure function of its arguments, but a host call of a
+// few microseconds; a decode step encodes 4-5 maps per layer per call, which made the
+// eager (e2e) path host-bound at c2.  Encoded maps are cached by their full argument
+// list (direct-mapped, 1024 entries, under a mutex): a hit is a key compare and a copy.
+struct MapKey {
+  void* addr;
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t box[5], estr[5];
+  uint32_t rank, dt, il, sw, l2, oob;
+};
+struct MapEntry {
+  MapKey key;
+  CUtensorMap map;
+  bool valid;
+};
+constexpr int kMapCache = 1024;
+MapEntry g_map_cache[kMapCache];
+std::mutex g_map_mu;
+
+CUresult encode_cached(CUtensorMap* out, CUtensorMapDataType dt, cuuint32_t rank, void* addr, const cuuint64_t* dims,
+                       const cuuint64_t* strides, const cuuint32_t* box, const cuuint32_t* estr,
+                       CUtensorMapInterleave il, CUtensorMapSwizzle sw, CUtensorMapL2promotion l2,
+                       CUtensorMapFloatOOBfill oob) {
+  if (rank < 1 || rank > 5) return g_encode_drv(out, dt, rank, addr, dims, strides, box, estr, il, sw, l2, oob);
+  MapKey k;
+  std::memset(&k, 0, sizeof(k));
+  k.addr = addr; k.rank = rank; k.dt = dt; k.il = il; k.sw = sw; k.l2 = l2; k.oob = oob;
+  for (uint32_t i = 0; i < rank; ++i) { k.dims[i] = dims[i]; k.box[i] = box[i]; k.estr[i] = estr[i]; }
+  for (uint32_t i = 0; i + 1 < rank; ++i) k.strides[i] = strides[i];
+  uint64_t h = 1469598103934665603ull;   // FNV-1a over the key bytes
+  const unsigned char* kb = reinterpret_cast<const unsigned char*>(&k);
+  for (size_t i = 0; i < sizeof(k); ++i) h = (h ^ kb[i]) * 1099511628211ull;
+  MapEntry& e = g_map_cache[h % kMapCache];
+  {
+    std::lock_guard<std::mutex> lock(g_map_mu);
+    if (e.valid && std::memcmp(&e.key, &k, sizeof(k)) == 0) { *out = e.map; return CUDA_SUCCESS; }
+  }
+  const CUresult r = g_encode_drv(out, dt, rank, addr, dims, strides, box, estr, il, sw, l2, oob);
+  if (r == CUDA_SUCCESS) {
+    std::lock_guard<std::mutex> lock(g_map_mu);
+    e.key = k; e.map = *out; e.valid = true;
+  }
+  return r;
+}
+
 bool get_encoder() {
   std::call_once(g_encode_once, [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        q == cudaDriverEntryPointSuccess) {
+      g_encode_drv = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+      g_encode = &encode_cached;
+    }
   });
   return g_encode != nullptr;
 }
@@ -480,9 +529,9 @@ sals_status launch_recon_attn_tc(const TcArgs& a, int batch, cudaStream_t st) {
       }
     }
     // (cta_group::2 variant) U boxes of 128 columns: one half of the pair's 256 per CTA
-    CUtensorMap mu2;
+    CUtensorMap mu2 = map;
     cuuint32_t box2[2] = {kBK, kBN / 2};
-    if (g_encode(&mu2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a.U), dims, strides, box2, estr,
+    if (tc2_pair_enabled() && g_encode(&mu2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a.U), dims, strides, box2, estr,
                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
       g_tc_err = "cuTensorMapEncodeTiled failed for the 128-column U map";

@@ -33,7 +33,8 @@ struct TcArgs {
 
 bool tc_supported(int head_dim, int D, int rank, int G);
 bool tc2_supported(int head_dim, int D, int rank, int G);   // persistent v2 (d = 128, G <= 4)
-int tc2_merge_max_splits(int G);                             // in-kernel split merge limit
+int tc2_merge_max_splits(int G);
+bool tc2_pair_enabled();                                       // SALS_TC2_CG=2: cta_group::2 MHA variant                             // in-kernel split merge limit
 sals_status launch_recon_attn_tc(const TcArgs& a, int batch, cudaStream_t st);
 const char* tc_last_error();
 // cuTensorMapEncodeTiled (driver entry point, resolved once), or nullptr.

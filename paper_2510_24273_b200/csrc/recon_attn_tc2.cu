@@ -143,8 +143,19 @@ __device__ __forceinline__ uint32_t mapa_rank(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
   return r;
 }
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+#ifndef SALS_RELAY_RELEASE
+#define SALS_RELAY_RELEASE 0
+#endif
+// relay / accumulator-release arrive: the stage's bytes were written by the async proxy
+// (TMA / cp.async) and are complete (the local full barrier), the TMEM reads of an
+// epilogue warp are complete (tcgen05.wait::ld); relaxed avoids a cluster-scope release
+// fence per arrive, measured ~1.3k cycles each (SALS_RELAY_RELEASE=1: the release form)
+__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint32_t cluster_addr) {
+#if SALS_RELAY_RELEASE
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+#else
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+#endif
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -523,7 +534,8 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
           const int s = u % ST;
           mbar_wait(&full[s], (u / ST) & 1);
           fence_proxy_async();   // the cp.async-written A rows -> the tensor core's proxy
-          mbar_arrive_remote(mapa_rank(&pfull[s], 0));
+          mbar_arrive_remote_relaxed(mapa_rank(&pfull[s], 0));
+          if (it == 0 && kc < 8) TSTAMP(96 + kc);
         }
     }
   } else if (warp == 1) {
@@ -727,7 +739,7 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
         tc_fence_after();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_remote(mapa_rank(&tempty[buf], 0));
+        if (lane == 0) mbar_arrive_remote_relaxed(mapa_rank(&tempty[buf], 0));   // (TMEM reads waited: wait::ld)
         continue;
       }
       const int nv = min(kRows, cnt - tile * kRows);
@@ -821,7 +833,7 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {                               // this warp is done with the accumulator
-          if constexpr (C2) mbar_arrive_remote(mapa_rank(&tempty[buf], 0));
+          if constexpr (C2) mbar_arrive_remote_relaxed(mapa_rank(&tempty[buf], 0));   // (TMEM reads waited: wait::ld)
           else mbar_arrive(&tempty[buf]);
         }
       }
@@ -1078,14 +1090,18 @@ cudaError_t launch_t(const CUtensorMap& map, const CUtensorMap& map_lat, const C
 // Opt-in (SALS_TC2_CG=2): parity-green but measured slower than the one-CTA kernel at c2
 // (profiles/r2/experiments).
 int tc2_pair_axis(const TcArgs& a, int batch) {
-  static const bool on = [] { const char* e = getenv("SALS_TC2_CG"); return e && e[0] == '2'; }();
-  if (!on || a.G != 1 || a.v_bits != 0) return 0;
+  if (!tc2_pair_enabled() || a.G != 1 || a.v_bits != 0) return 0;
   if (a.ntiles % 2 == 0) return 1;
   if (batch % 2 == 0) return 3;
   return 0;
 }
 
 }  // namespace tc2
+
+bool tc2_pair_enabled() {
+  static const bool on = [] { const char* e = getenv("SALS_TC2_CG"); return e && e[0] == '2'; }();
+  return on;
+}
 
 extern "C" int sals_debug_tc_ctatime(unsigned long long* host_out) {
 #ifdef SALS_TC_CTATIME

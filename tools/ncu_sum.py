@@ -11,7 +11,8 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "TPC.TriageCompute.sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg",
         "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
         "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
-        "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active", "gpc__cycles_elapsed.max"]
+        "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active", "gpc__cycles_elapsed.max",
+        "l1tex__m_xbar2l1tex_read_bytes.sum", "lts__t_sectors.sum", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"]
 for rep in sys.argv[1:]:
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(raw.splitlines()))

@@ -28,4 +28,5 @@ t0 = t[80]
 names = {0: "mma_start", 88: "pfull0(cg2)", 8: "mma_commit", 16: "epi_tfull", 24: "epi_logits", 32: "epi_vfull", 40: "epi_pvdone", 64: "a_first_iss", 72: "a_last_iss"}
 for base, nm in names.items():
     print(f"{nm:12s}", " ".join(f"{(t[base+i]-t0)/1000:8.2f}" for i in range(4)), " kcycles")
+print("relay(cg2,t0) ", " ".join(f"{(t[96+i]-t0)/1000:7.2f}" for i in range(8)))
 print("after_wait", (t[82]-t0)/1000, "end", (t[81]-t0)/1000)
