@@ -322,6 +322,20 @@ sals_status sals_decode_sharded(const sals_config* cfg, void* comm, const void* 
                                 int32_t batch, int64_t shard_start, const int32_t* d_local_len,
                                 int32_t max_local_len, const int32_t* d_seq_len, void* out,
                                 void* workspace, size_t ws_bytes, void* stream);
+/* The sharded layer-step with the new token's append (Alg. 1 lines 2-3)
+ * in the same call, as sals_append_decode is for one GPU: every rank passes
+ * k_new / v_new [B, D]; the rank whose shard holds the newest position of request b
+ * (shard_start + d_local_len[b] - 1 == d_seq_len[b] - 1, its last local row) writes
+ * U^T k_new and v_new into that row inside the query projection's launch (one read
+ * of U), the others write nothing.  d_local_len / d_seq_len already count the new
+ * token.  Equivalent to sals_append_latent(pos = d_local_len - 1) on that rank
+ * followed by sals_decode_sharded; same workspace, errors and limits. */
+sals_status sals_append_decode_sharded(const sals_config* cfg, void* comm, const void* U, const void* k_new,
+                                       const void* v_new, const void* q, void* latent_shard, void* v_shard,
+                                       int64_t cap_local, int32_t batch, int64_t shard_start,
+                                       const int32_t* d_local_len, int32_t max_local_len,
+                                       const int32_t* d_seq_len, void* out, void* workspace, size_t ws_bytes,
+                                       void* stream);
 
 const char* sals_status_string(sals_status s);
 const char* sals_last_error(void);

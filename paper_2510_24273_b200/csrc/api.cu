@@ -884,11 +884,14 @@ size_t sals_shard_workspace_bytes(const sals_config* cfg, int32_t batch, int32_t
   return align_up(p.total, 256);
 }
 
-sals_status sals_shard_candidates(const sals_config* cfg, const void* U, const void* q, const void* latent_shard,
-                                  int64_t cap_local, int32_t batch, int64_t shard_start,
-                                  const int32_t* d_local_len, int32_t max_local_len, const int32_t* d_seq_len,
-                                  float* cand_score, int32_t* cand_idx, void* workspace, size_t ws_bytes,
-                                  void* stream) {
+// (k_new != nullptr: the new token's latent / value rows are appended in the query
+// projection's launch, on the shard that holds position s_b - 1; sals_append_decode_sharded)
+static sals_status shard_candidates_impl(const sals_config* cfg, const void* U, const void* q,
+                                         const void* latent_shard, int64_t cap_local, int32_t batch,
+                                         int64_t shard_start, const int32_t* d_local_len, int32_t max_local_len,
+                                         const int32_t* d_seq_len, float* cand_score, int32_t* cand_idx,
+                                         void* workspace, size_t ws_bytes, void* stream, const void* k_new,
+                                         const void* v_new, void* v_shard) {
   sals_status s = validate(cfg);
   if (s != SALS_OK) return s;
   if (!U || !q || !latent_shard || !d_local_len || !d_seq_len || !cand_score || !cand_idx || !workspace)
@@ -911,15 +914,24 @@ sals_status sals_shard_candidates(const sals_config* cfg, const void* U, const v
   pa.rope = make_rope(cfg);
   uint32_t* hist = reinterpret_cast<uint32_t*>(ws + p.off_hist);
   pa.hist0_zero = hist; pa.hist0_words = p.hist_words;
+  const bool fused = k_new != nullptr;
+  if (fused) {   // append role in the same launch: one read of U (as sals_append_decode)
+    pa.xa = k_new; pa.ncols_a = cfg->rank; pa.v_new = v_new; pa.pos = nullptr;
+    pa.v_bits = vq_bits(cfg); pa.v_row_bytes = (int)v_row_bytes(cfg);
+    pa.latent = const_cast<void*>(latent_shard); pa.v_cache = v_shard; pa.cap = cap_local;
+    pa.append_len = d_local_len; pa.append_base = shard_start;
+  }
+  const int mode = fused ? 2 : 1;
   ScoreArgs sa{};
   sa.latent = latent_shard; sa.cap = cap_local; sa.r = cfg->rank; sa.rstar = cfg->score_rank; sa.qtil = qtil;
   sa.len = d_local_len; sa.scores = scores; sa.stride = p.score_stride;
   sa.hist0 = hist; sa.seq_len = d_seq_len; sa.idx_base = shard_start; sa.sink = cfg->sink; sa.recent = cfg->recent;
+  sa.stream_after_wait = fused ? 1 : 0;   // the new latent row comes from the kernel just before
   if (cfg->dtype == SALS_BF16) {
-    if (on(kStQproj)) s = launch_project<__nv_bfloat16>(cfg, p, 1, pa, st);
+    if (on(kStQproj)) s = launch_project<__nv_bfloat16>(cfg, p, mode, pa, st);
     if (s == SALS_OK && on(kStScore)) s = launch_score<__nv_bfloat16>(cfg, sa, batch, max_local_len, st);
   } else {
-    if (on(kStQproj)) s = launch_project<float>(cfg, p, 1, pa, st);
+    if (on(kStQproj)) s = launch_project<float>(cfg, p, mode, pa, st);
     if (s == SALS_OK && on(kStScore)) s = launch_score<float>(cfg, sa, batch, max_local_len, st);
   }
   if (s != SALS_OK) return s;
@@ -931,6 +943,16 @@ sals_status sals_shard_candidates(const sals_config* cfg, const void* U, const v
   ta.sel_count = reinterpret_cast<int*>(ws + p.off_ccount);   // read by the selection (shard.cu)
   ta.hist0 = hist;
   return on(kStTopk) ? launch_topk(ta, batch, p, st) : SALS_OK;
+}
+
+sals_status sals_shard_candidates(const sals_config* cfg, const void* U, const void* q, const void* latent_shard,
+                                  int64_t cap_local, int32_t batch, int64_t shard_start,
+                                  const int32_t* d_local_len, int32_t max_local_len, const int32_t* d_seq_len,
+                                  float* cand_score, int32_t* cand_idx, void* workspace, size_t ws_bytes,
+                                  void* stream) {
+  return shard_candidates_impl(cfg, U, q, latent_shard, cap_local, batch, shard_start, d_local_len, max_local_len,
+                               d_seq_len, cand_score, cand_idx, workspace, ws_bytes, stream, nullptr, nullptr,
+                               nullptr);
 }
 
 sals_status sals_shard_attend(const sals_config* cfg, const void* U, const void* q, const void* latent_shard,
@@ -1083,11 +1105,11 @@ size_t sals_decode_sharded_workspace_bytes(const sals_config* cfg, int32_t batch
   return shard_layout(cfg, batch, max_local_len, world).total;
 }
 
-sals_status sals_decode_sharded(const sals_config* cfg, void* comm, const void* U, const void* q,
-                                const void* latent_shard, const void* v_shard, int64_t cap_local, int32_t batch,
-                                int64_t shard_start, const int32_t* d_local_len, int32_t max_local_len,
-                                const int32_t* d_seq_len, void* out, void* workspace, size_t ws_bytes,
-                                void* stream) {
+static sals_status decode_sharded_impl(const sals_config* cfg, void* comm, const void* U, const void* q,
+                                       const void* latent_shard, const void* v_shard, int64_t cap_local,
+                                       int32_t batch, int64_t shard_start, const int32_t* d_local_len,
+                                       int32_t max_local_len, const int32_t* d_seq_len, void* out, void* workspace,
+                                       size_t ws_bytes, void* stream, const void* k_new, const void* v_new) {
   sals_status s = validate(cfg);
   if (s != SALS_OK) return s;
   // everything the later phases check, checked before the first one enqueues work
@@ -1111,8 +1133,9 @@ sals_status sals_decode_sharded(const sals_config* cfg, void* comm, const void* 
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   // 1. local candidates: scores straight into this rank's slot of the gather buffer,
   //    global indices kept locally (the gathered order (rank, position) is the index order)
-  s = sals_shard_candidates(cfg, U, q, latent_shard, cap_local, batch, shard_start, d_local_len, max_local_len,
-                            d_seq_len, cand_s + me * nc, cand_i, workspace, L.base, stream);
+  s = shard_candidates_impl(cfg, U, q, latent_shard, cap_local, batch, shard_start, d_local_len, max_local_len,
+                            d_seq_len, cand_s + me * nc, cand_i, workspace, L.base, stream, k_new, v_new,
+                            const_cast<void*>(v_shard));
   if (s != SALS_OK) return s;
   // 2. in-place all-gather of the candidate scores (rank order)
   if (on(kStExchange)) SALS_NCCL_TRY(nccl().all_gather(cand_s + me * nc, cand_s, nc, ncclFloat32, c->comm, st));
@@ -1123,6 +1146,25 @@ sals_status sals_decode_sharded(const sals_config* cfg, void* comm, const void* 
   // 4. in-place all-gather of the partials, 5. merge on every rank
   if (on(kStExchange)) SALS_NCCL_TRY(nccl().all_gather(part_all + me * np, part_all, np, ncclFloat32, c->comm, st));
   return on(kStMerge) ? sals_merge_partials(cfg, part_all, P, batch, out, stream) : SALS_OK;
+}
+
+sals_status sals_decode_sharded(const sals_config* cfg, void* comm, const void* U, const void* q,
+                                const void* latent_shard, const void* v_shard, int64_t cap_local, int32_t batch,
+                                int64_t shard_start, const int32_t* d_local_len, int32_t max_local_len,
+                                const int32_t* d_seq_len, void* out, void* workspace, size_t ws_bytes,
+                                void* stream) {
+  return decode_sharded_impl(cfg, comm, U, q, latent_shard, v_shard, cap_local, batch, shard_start, d_local_len,
+                             max_local_len, d_seq_len, out, workspace, ws_bytes, stream, nullptr, nullptr);
+}
+
+sals_status sals_append_decode_sharded(const sals_config* cfg, void* comm, const void* U, const void* k_new,
+                                       const void* v_new, const void* q, void* latent_shard, void* v_shard,
+                                       int64_t cap_local, int32_t batch, int64_t shard_start,
+                                       const int32_t* d_local_len, int32_t max_local_len, const int32_t* d_seq_len,
+                                       void* out, void* workspace, size_t ws_bytes, void* stream) {
+  if (!k_new || !v_new) return fail(SALS_ERR_INVALID_ARGUMENT, "NULL tensor argument");
+  return decode_sharded_impl(cfg, comm, U, q, latent_shard, v_shard, cap_local, batch, shard_start, d_local_len,
+                             max_local_len, d_seq_len, out, workspace, ws_bytes, stream, k_new, v_new);
 }
 
 }  // extern "C"

@@ -37,6 +37,9 @@ struct ProjectArgs {
   // fused append + query projection (MODE 2): append role's input / columns / block count;
   // pos == nullptr -> the new token's slot is seq_len[b] - 1
   const void* xa; int ncols_a; int n_append_blocks;
+  // (sharded) append_len != nullptr: the new token's local slot is seq_len[b] - 1 - append_base,
+  // written only when it is this shard's last row (append_len[b] - 1), else skipped
+  const int* append_len; int64_t append_base;
   int v_bits, v_row_bytes;   // value row format (0: dtype values; 4 / 2: quantised, head_dim 128)
   int hp_window;             // > 0: the last hp_window tokens also kept at 8 bits in a ring after the main rows
   int64_t hp_ring_off;       // bytes from v_cache to the ring [B, hp_window, n_kv * 144]

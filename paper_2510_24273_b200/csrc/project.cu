@@ -35,6 +35,15 @@ constexpr int kProjUnroll = 8;    // row loads in flight per lane
 // (+ query RoPE role, histogram zeroing); 2: both in one launch (sals_append_decode):
 // blockIdx.y < n_append_blocks are append column blocks, the rest the query role.
 // NT threads: 512 when a CTA owns 512 rows of U (D = 4096), else 256 (measured)
+// Slot of request b's new token in the cache this call appends to, or -1 when this call
+// does not append it (a sequence shard that does not hold position seq_len[b] - 1).
+__device__ __forceinline__ int append_slot(const ProjectArgs& a, int b) {
+  if (a.pos) return a.pos[b];
+  const int slot = a.seq_len[b] - 1 - (int)a.append_base;
+  if (a.append_len && (slot < 0 || slot != a.append_len[b] - 1)) return -1;
+  return slot;
+}
+
 template <typename T, int MODE, int NT>
 __global__ void __launch_bounds__(NT, SALS_PROJ_MINB)   // 2: <= 128 registers, co-resident with the next kernel
 project_kernel(ProjectArgs a) {
@@ -146,8 +155,9 @@ project_kernel(ProjectArgs a) {
       const int nvec = a.D * (int)sizeof(T) / 16;
       for (int i = cta * NT + tid; i < a.B * nvec; i += ncta * NT) {
         const int b = i / nvec, v = i % nvec;
+        const int pb = append_slot(a, b);
+        if (pb < 0) continue;
         const uint4 val = ld_v4(reinterpret_cast<const char*>(a.v_new) + ((size_t)b * a.D) * sizeof(T) + v * 16);
-        const int pb = a.pos ? a.pos[b] : a.seq_len[b] - 1;
         *reinterpret_cast<uint4*>(reinterpret_cast<char*>(a.v_cache) +
                                   (((size_t)b * a.cap + pb) * a.D) * sizeof(T) + v * 16) = val;
       }
@@ -160,13 +170,14 @@ project_kernel(ProjectArgs a) {
       const int nitems = a.B * (a.D / 8);             // (request, 8-channel slice); 4 per group, lane-adjacent
       for (int i0 = cta * NT; i0 < nitems; i0 += ncta * NT) {
         const int i = i0 + tid;
-        const bool ok = i < nitems;
-        const int b = ok ? i / (a.D / 8) : 0, sl = ok ? i - b * (a.D / 8) : 0;
+        const int b = i < nitems ? i / (a.D / 8) : 0;
+        const int pb = i < nitems ? append_slot(a, b) : 0;
+        const bool ok = i < nitems && pb >= 0;   // (the quantiser's lane groups stay whole: a request is all in or out)
+        const int sl = i < nitems ? i - b * (a.D / 8) : 0;
         const int gi = sl >> 2, q = sl & 3, h = gi / gph, gq = gi - h * gph;
         float f[8];
         if (ok) Elem<__nv_bfloat16>::unpack(ld_v4(reinterpret_cast<const char*>(a.v_new) + ((size_t)b * a.D + sl * 8) * 2), f);
         else for (int e = 0; e < 8; ++e) f[e] = 0.f;
-        const int pb = ok ? (a.pos ? a.pos[b] : a.seq_len[b] - 1) : 0;
         char* row = reinterpret_cast<char*>(a.v_cache) + ((size_t)b * a.cap + pb) * a.v_row_bytes + (size_t)h * hb;
         char* ring = a.hp_window > 0
                          ? reinterpret_cast<char*>(a.v_cache) + a.hp_ring_off +
@@ -297,8 +308,8 @@ project_kernel(ProjectArgs a) {
           a.out_f32[(size_t)b * ncols + cj] = sum;
         } else {
           T* lat = reinterpret_cast<T*>(a.latent);
-          const int pb = a.pos ? a.pos[b] : a.seq_len[b] - 1;
-          lat[((size_t)b * a.cap + pb) * a.r + cj] = Elem<T>::from_f(sum);
+          const int pb = append_slot(a, b);
+          if (pb >= 0) lat[((size_t)b * a.cap + pb) * a.r + cj] = Elem<T>::from_f(sum);
         }
       }
     }

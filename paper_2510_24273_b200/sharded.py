@@ -130,12 +130,12 @@ def bench(args, rank, world):
 
     def step():
         for i, ly in enumerate(layers):
-            if owner:
-                sals.sals_append_latent(cfg, ly["U"], ly["k_new"], ly["v_new"], pos_local, ly["latent"], ly["v"])
-            if comm is not None:
-                sals.sals_decode_sharded(cfg, comm, ly["U"], ly["q"], ly["latent"], ly["v"], start, loc, n_loc, seq,
-                                         outs[i], ws)
+            if comm is not None:   # the append runs inside the call, on the rank holding position s - 1
+                sals.sals_append_decode_sharded(cfg, comm, ly["U"], ly["k_new"], ly["v_new"], ly["q"], ly["latent"],
+                                                ly["v"], start, loc, n_loc, seq, outs[i], ws)
             else:
+                if owner:
+                    sals.sals_append_latent(cfg, ly["U"], ly["k_new"], ly["v_new"], pos_local, ly["latent"], ly["v"])
                 decs[i].decode(ly["latent"], ly["v"], start, loc)
 
     stream = torch.cuda.Stream()
@@ -211,12 +211,12 @@ def bench(args, rank, world):
                 "config": {"workload": f"c4-sharded: B={B} n={s} sequence-sharded over {world} GPUs x{L} layers",
                            "batch": B, "seq_len": s, "layers": L, "parallelism": f"sequence-shard x{world}",
                            "graph": graph is not None,
-                           "exchange": "sals_decode_sharded (library NCCL)" if comm is not None
+                           "exchange": "sals_append_decode_sharded (library NCCL; the append in the query projection's launch)" if comm is not None
                            else "torch.distributed all_gather_into_tensor"},
                 "us_per_layer_step": ms * 1e3 / L,
                 "phases_us_per_layer": phases,
                 "phases_note": "graph of the step with one phase enabled (others skipped), max over ranks; "
-                               "'append' is the owner rank's sals_append_latent, 'exchange' the two NCCL all-gathers"}
+                               "'qproj_rope' includes the owner rank's append (one launch), 'exchange' the two NCCL all-gathers"}
         print(json.dumps(line), flush=True)
     if comm is not None:
         torch.cuda.synchronize()

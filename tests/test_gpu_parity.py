@@ -416,6 +416,45 @@ def test_decode_sharded_nccl_one_rank(sink, recent):
         sals.sals_comm_destroy(comm)
 
 
+def test_append_decode_sharded_one_rank():
+    """sals_append_decode_sharded on a one-rank communicator: the appended latent row
+    (U^T k_new, 1 bf16 ulp) and value row (bit-exact) against the oracle, the output
+    against the oracle forced to the selection of the unsharded fused call on the same
+    problem; a shard that does not hold position s - 1 writes nothing."""
+    from paper_2510_24273_b200 import sals
+    sh = _shape("c4", rank=256, score_rank=128, top_k=1024)
+    B, s = 2, 20000
+    seqs = [s, s - 3333]
+    cfg, host, gpu = H.run_sals(sh, B, seqs, seed=41, fused=True)
+    oc = H.oracle_cfg(sh, 0, 0)
+    p = synth.gen_problem(num_q_heads=sh["num_q_heads"], num_kv_heads=sh["num_kv_heads"], head_dim=sh["head_dim"],
+                          rank=sh["rank"], batch=B, seq_lens=seqs, cap=s, seed=41)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda().bfloat16()
+    U, q, kn, vn = dev(p["U"]), dev(p["q"]), dev(p["k_new"]), dev(p["v_new"])
+    lat, vv = dev(p["latent"]), dev(p["v"])
+    seq = torch.tensor(seqs, dtype=torch.int32, device="cuda")
+    comm = sals.sals_comm_init(sals.sals_comm_unique_id(), 1, 0)
+    try:
+        ws = sals.alloc_workspace(sals.sals_decode_sharded_workspace_bytes(cfg, B, s, 1), "cuda")
+        out = torch.empty(B, sh["num_q_heads"] * sh["head_dim"], dtype=torch.bfloat16, device="cuda")
+        sals.sals_append_decode_sharded(cfg, comm, U, kn, vn, q, lat, vv, 0, seq, s, seq, out, ws)
+        torch.cuda.synchronize()
+        hl, hv = H.widen(lat), H.widen(vv)
+        H.check_append(dict(U=H.widen(U), k_new=H.widen(kn), v_new=H.widen(vn), latent=hl, v=hv,
+                            seq_len=np.asarray(seqs)), "bf16")
+        forced = [gpu["sel"][b][gpu["sel"][b] >= 0].astype(np.int64) for b in range(B)]
+        orc = O.decode(oc, H.widen(U), H.widen(q), hl, hv, np.asarray(seqs), forced_selection=forced)
+        H.check_output(H.widen(out), orc["y"], "bf16")
+        # a shard holding positions [0, s_b - 100) is not the newest token's owner: no write
+        lat2, v2 = dev(p["latent"]), dev(p["v"])
+        loc = (seq - 100).to(torch.int32)
+        sals.sals_append_decode_sharded(cfg, comm, U, kn, vn, q, lat2, v2, 0, loc, s, seq, out, ws)
+        torch.cuda.synchronize()
+        assert torch.equal(lat2, dev(p["latent"])) and torch.equal(v2, dev(p["v"]))
+    finally:
+        sals.sals_comm_destroy(comm)
+
+
 # ------------------------------------------------------------------ fused append + decode
 @pytest.mark.parametrize("nkv,G,d,B,seqs", [(8, 4, 128, 3, [3000, 1777, 2048]),   # D = 1024
                                           (32, 1, 128, 2, [4096, 2500])])         # D = 4096
