@@ -103,6 +103,124 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tma_kernel(const __grid_con
         bulk_load(smem_u32(dst + kStageBytes), vb + (size_t)u * ts * rowb, bytes, &full[s], pol);
       }
     }
+  } else if constexpr (G == 4 && HPW == 1) {
+    // ================= consumers, GQA 4 (c3 / c4): transposed reductions =================
+    // Lane (sub, li) holds dims [8 li, +8) of the 4 token pairs' tokens 2 i + sub.  The 16
+    // partial logits (pair i, query head g) of a lane are reduced over the 16 lanes of its
+    // half with a TRANSPOSING butterfly (15 shuffles instead of 64: each level halves the
+    // values a lane keeps), after which lane li holds the full logit of (i, g) = (li / 4,
+    // li % 4).  The online softmax then runs one value per lane (group max / sum over the 8
+    // lanes of query head g: 3 shuffles each), the rescale factors and the 16 p are
+    // broadcast back for the P V.  m and l of head g are kept (group-uniform) by the lanes
+    // with li % 4 == g; o by every lane for its 8 dims and its token parity.
+    pdl_wait();   // q^R comes from the RoPE kernel just before
+    const int sub = lane >> 4, li = lane & 15;
+    const int hoff = warp * kDH * 2;
+    float2 q2[4][4], o2[4][4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const float4* qv = reinterpret_cast<const float4*>(a.qrope + ((size_t)b * a.n_q + warp * 4 + g) * kDH + li * 8);
+      const float4 q0 = qv[0], q1 = qv[1];
+      const float sl = a.scale_log2;
+      q2[g][0] = make_float2(q0.x * sl, q0.y * sl); q2[g][1] = make_float2(q0.z * sl, q0.w * sl);
+      q2[g][2] = make_float2(q1.x * sl, q1.y * sl); q2[g][3] = make_float2(q1.z * sl, q1.w * sl);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) o2[g][e] = make_float2(0.f, 0.f);
+    }
+    float m_s = -INFINITY, l_s = 0.f;   // query head li % 4 (group-uniform)
+    const int src_half = lane & 16;
+    for (int u = 0; u < nst; ++u) {
+      const int s = u % kStages;
+      const int nt = min(ts, t1 - (t0 + u * ts));
+      mbar_wait(&full[s], (u / kStages) & 1);
+      const uint8_t* ks = smem + (size_t)s * 2 * kStageBytes + li * 16 + hoff;
+      const uint8_t* vs = ks + kStageBytes;
+      uint4 kr[4], vr[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int t = 2 * i + sub;
+        kr[i] = t < nt ? *reinterpret_cast<const uint4*>(ks + t * rowb) : make_uint4(0, 0, 0, 0);
+        vr[i] = t < nt ? *reinterpret_cast<const uint4*>(vs + t * rowb) : make_uint4(0, 0, 0, 0);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);   // the stage is in registers
+      float v[16];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t w[4] = {kr[i].x, kr[i].y, kr[i].z, kr[i].w};
+        float2 k2[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) k2[e] = make_float2(__uint_as_float(w[e] << 16), __uint_as_float(w[e] & 0xffff0000u));
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          float2 acc = __fmul2_rn(q2[g][0], k2[0]);
+#pragma unroll
+          for (int e = 1; e < 4; ++e) acc = __ffma2_rn(q2[g][e], k2[e], acc);
+          v[i * 4 + g] = acc.x + acc.y;
+        }
+      }
+#pragma unroll
+      for (int off = 8, c = 8; off > 0; off >>= 1, c >>= 1) {
+        const bool up = (li & off) != 0;
+#pragma unroll
+        for (int k = 0; k < c; ++k) {
+          const float send = up ? v[k] : v[k + c];
+          const float keep = up ? v[k + c] : v[k];
+          v[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+      }
+      const bool valid = 2 * (li >> 2) + sub < nt;
+      const float sc = valid ? v[0] : -INFINITY;
+      float mx = sc;
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+      const float mn = fmaxf(m_s, mx);   // (token 0 of a stage is always valid: mn finite)
+      const float alpha = m_s == -INFINITY ? 0.f : exp2f(m_s - mn);
+      const float p = valid ? exp2f(sc - mn) : 0.f;
+      float ps = p + __shfl_xor_sync(0xffffffffu, p, 4);
+      ps += __shfl_xor_sync(0xffffffffu, ps, 8);
+      ps += __shfl_xor_sync(0xffffffffu, ps, 16);
+      l_s = l_s * alpha + ps;
+      m_s = mn;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const float al = __shfl_sync(0xffffffffu, alpha, src_half | g);
+        const float2 al2 = make_float2(al, al);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) o2[g][e] = __fmul2_rn(o2[g][e], al2);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t w[4] = {vr[i].x, vr[i].y, vr[i].z, vr[i].w};
+        float2 v2[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v2[e] = make_float2(__uint_as_float(w[e] << 16), __uint_as_float(w[e] & 0xffff0000u));
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const float pg = __shfl_sync(0xffffffffu, p, src_half | (4 * i + g));
+          const float2 p2 = make_float2(pg, pg);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) o2[g][e] = __ffma2_rn(p2, v2[e], o2[g][e]);
+        }
+      }
+    }
+    // the two token parities share m: add their o; write the partials (lanes of half 0)
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      float ov[8];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        ov[2 * e] = o2[g][e].x + __shfl_xor_sync(0xffffffffu, o2[g][e].x, 16);
+        ov[2 * e + 1] = o2[g][e].y + __shfl_xor_sync(0xffffffffu, o2[g][e].y, 16);
+      }
+      float* dst = a.partials + (((size_t)b * a.n_q + warp * 4 + g) * a.nsplit + split) * (kDH + 2);
+      if (sub == 0) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) dst[2 + li * 8 + e] = ov[e];
+        if (li == g) { dst[0] = m_s; dst[1] = l_s; }
+      }
+    }
   } else {
     // ================= consumers =================
     pdl_wait();   // q^R comes from the RoPE kernel just before
@@ -231,9 +349,9 @@ __global__ void __launch_bounds__(kThreads, 1) dense_tma_kernel(const __grid_con
 // Measured (bench dense step, round 2): with 8 KV heads (D = 1024, the GQA shapes c3 / c4)
 // this kernel beats flash_decode_kernel (c4 0.50 vs 0.42 of the HBM peak); with 32
 // heads (D = 4096, c2) flash_decode_kernel's 8-heads-per-CTA LSU stream is faster
-// (0.92 vs 0.84), so the TMA kernel is built for n_kv = 8 only.
+// (0.92 vs 0.84), so the TMA kernel is built for n_kv = 8 only (G <= 4: registers).
 bool dense_tma_supported(int head_dim, int n_kv, int G, int dtype_bytes) {
-  return dtype_bytes == 2 && head_dim == dtma::kDH && n_kv == dtma::kCons && (G == 1 || G == 2 || G == 4 || G == 8);
+  return dtype_bytes == 2 && head_dim == dtma::kDH && n_kv == dtma::kCons && (G == 1 || G == 2 || G == 4);
 }
 
 void dense_tma_plan(int batch, int max_len, int head_dim, int n_kv, int nsm, int& nsplit, int& chunk) {
@@ -252,10 +370,10 @@ cudaError_t launch_dense_tma(const FlashArgs& a, int batch, int head_dim, int G,
   int ki = 0;
 #define SALS_DT_CASE(H, GG, I) \
   if (hpw == H && G == GG) { k = dtma::dense_tma_kernel<GG, H>; ki = I; }
-  SALS_DT_CASE(1, 1, 0) SALS_DT_CASE(1, 2, 1) SALS_DT_CASE(1, 4, 2) SALS_DT_CASE(1, 8, 3)
+  SALS_DT_CASE(1, 1, 0) SALS_DT_CASE(1, 2, 1) SALS_DT_CASE(1, 4, 2)
 #undef SALS_DT_CASE
   if (!k) return cudaErrorNotSupported;
-  static DeviceOnce once[4];
+  static DeviceOnce once[3];
   cudaError_t e = once[ki].run(
       [&] { return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dtma::kSmem); });
   if (e != cudaSuccess) return e;

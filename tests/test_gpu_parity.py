@@ -229,7 +229,7 @@ def test_dense_decode(dtype, G):
 @pytest.mark.parametrize("nkv,G,B,cap,lens", [
     (8, 4, 4, 3000, [3000, 1, 1777, 9]),        # D = 1024 (c3 / c4 heads): TMA kernel, 8 tokens per stage
     (8, 2, 3, 2051, [2051, 2, 1000]),
-    (8, 8, 2, 999, [999, 31]),
+    (8, 8, 2, 999, [999, 31]),                  # G = 8: flash_decode_kernel
     (8, 1, 2, 40000, [40000, 33333]),           # long rows: many stages per CTA
     (32, 1, 3, 1025, [1025, 1, 513]),           # D = 4096 (c2 heads): flash_decode_kernel
 ])
