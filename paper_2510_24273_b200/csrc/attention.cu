@@ -302,18 +302,30 @@ __global__ void merge_kernel(MergeArgs a) {
     }
     __syncthreads();
     const float M = s_M, L = s_L;
-    for (int i = threadIdx.x; i < a.head_dim; i += blockDim.x) {
+    // blockDim = head_dim x SG: thread (sg, i) sums the splits sg, sg + SG, ... of dim i
+    // (SG independent load streams per dim, launch_merge picks SG from nsplit); the SG
+    // partial sums meet in shared memory, summed in sg order (deterministic)
+    const int SG = max(1, (int)blockDim.x / a.head_dim);
+    const int sg = threadIdx.x / a.head_dim;
+    const int i = threadIdx.x - sg * a.head_dim;
+    __shared__ float s_part[3][256];
+    float acc = 0.f;
+    if (sg < SG) {
       const float* po = base + 2 + i;
-      float acc = 0.f;
-      int s = 0;
-      for (; s + 8 <= a.nsplit; s += 8) {
+      int s = sg;
+      for (; s + 7 * SG < a.nsplit; s += 8 * SG) {
         float ov[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) ov[j] = po[(size_t)(s + j) * a.s_stride];
+        for (int j = 0; j < 8; ++j) ov[j] = po[(size_t)(s + j * SG) * a.s_stride];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc = fmaf(sw[s + j], ov[j], acc);
+        for (int j = 0; j < 8; ++j) acc = fmaf(sw[s + j * SG], ov[j], acc);
       }
-      for (; s < a.nsplit; ++s) acc = fmaf(sw[s], po[(size_t)s * a.s_stride], acc);
+      for (; s < a.nsplit; s += SG) acc = fmaf(sw[s], po[(size_t)s * a.s_stride], acc);
+      if (sg > 0) s_part[sg - 1][i] = acc;
+    }
+    __syncthreads();
+    if (sg == 0) {
+      for (int k = 0; k < SG - 1; ++k) acc += s_part[k][i];
       if (a.normalize) {
         T* out = reinterpret_cast<T*>(a.out) + ((size_t)b * a.n_q + h) * a.head_dim;
         out[i] = Elem<T>::from_f(L > 0.f ? acc / L : 0.f);
