@@ -3,20 +3,23 @@
 // attention reads 2 s d elements"; Eq. 6 with every token selected).
 //
 // The stage is a pure HBM stream of 2 B s D 2 bytes, so the design goal is
-// bytes in flight at minimum instruction cost (same recipe as score_tma.cu):
+// bytes in flight at minimum instruction cost (same recipe as score_tma.cu).
+// Built for the GQA shapes with 8 KV heads (c3 / c4: D = 1024, G <= 4; other shapes
+// use flash_decode_kernel, see dense_tma_supported):
 //  - one CTA per SM: grid (nsplit, B) with nsplit * B ~ #SMs; a CTA owns the
 //    contiguous token range [split * chunk, +chunk) of request b and ALL KV heads,
 //    so its K rows (and its V rows) are ONE contiguous byte range of the cache
 //    ([b, t, :] rows of D * 2 bytes are adjacent for consecutive t);
 //  - one producer lane streams that range with 1-D bulk copies
-//    (cp.async.bulk, 16 KB of K + 16 KB of V per stage = ts = 8192 / D tokens)
-//    into a 6-stage mbarrier ring (~160 KB in flight per SM);
-//  - 8 consumer warps: warp w owns KV heads {w + 8 j, j < HPW}; lane (sub, li)
-//    reads dims [8 li, 8 li + 8) of token 2 i + sub of the stage (one 16-byte
-//    shared-memory vector per token and head, conflict-free), holds the rotated
-//    queries of the G query heads of each owned KV head in registers, and keeps
-//    one online-softmax state (m, l, o[8]) per query head (log2 domain); the two
-//    token streams (sub = 0 / 1) are merged once at the end;
+//    (cp.async.bulk, 16 KB of K + 16 KB of V per stage = 8 tokens) into a 6-stage
+//    mbarrier ring (~160 KB in flight per SM), L2 evict-first;
+//  - 8 consumer warps, warp w = KV head w; lane (sub, li) reads dims [8 li, 8 li + 8)
+//    of token 2 i + sub of the stage (one 16-byte shared-memory vector per token,
+//    conflict-free) and holds the rotated queries of the G query heads in registers.
+//    G = 4: FFMA2 dot products, a transposing shuffle reduction (lane li ends with the
+//    logit of (pair li / 4, head li % 4)), the online softmax on one value per lane,
+//    FFMA2 P V; G = 1 / 2: a butterfly per (pair, head) and one online-softmax state
+//    (m, l, o[8]) per query head and token parity, merged at the end;
 //  - output: partials [B, n_q, nsplit, d+2] = (m, l, o[d]) for merge_kernel.
 // Programmatic dependent launch: the producer streams every stage that does not
 // hold the newest token (slot len - 1) before griddepcontrol.wait (the cache rows
