@@ -987,6 +987,42 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
         if constexpr (HPW) {
           if (tb + 16 <= thp) pv(std::false_type{});
           else pv(std::true_type{});
+        } else if constexpr (VB == 16) {
+          if (tb + 16 <= nv) {
+            // all 16 of the warp's tokens valid (every full tile): no per-token guards, the
+            // V vectors and probabilities of 8 tokens are loaded before their FFMA2s
+#pragma unroll
+            for (int h8 = 0; h8 < 2; ++h8) {
+              uint4 vr[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) vr[j] = vrow[(tb + 8 * h8 + j) * 32];
+              float4 pa[G], pb[G];
+#pragma unroll
+              for (int g = 0; g < G; ++g) {
+                pa[g] = *reinterpret_cast<const float4*>(pp + g * kPS + tb + 8 * h8);
+                pb[g] = *reinterpret_cast<const float4*>(pp + g * kPS + tb + 8 * h8 + 4);
+              }
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const uint32_t w[4] = {vr[j].x, vr[j].y, vr[j].z, vr[j].w};
+                float2 vv[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) vv[e] = make_float2(__uint_as_float(w[e] << 16), __uint_as_float(w[e] & 0xffff0000u));
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                  const float4 p4 = j < 4 ? pa[g] : pb[g];
+                  const int jj = j & 3;
+                  const float pj = jj == 0 ? p4.x : jj == 1 ? p4.y : jj == 2 ? p4.z : p4.w;
+                  lp[g] += pj;
+                  const float2 p2 = make_float2(pj, pj);
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) ov[g][e] = __ffma2_rn(p2, vv[e], ov[g][e]);
+                }
+              }
+            }
+          } else {
+            pv(std::false_type{});
+          }
         } else {
           pv(std::false_type{});
         }
