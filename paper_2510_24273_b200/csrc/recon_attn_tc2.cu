@@ -18,6 +18,15 @@
 //                 staged V rows.  Logits and K_C never leave the SM.
 // After its last tile the CTA writes y directly (single chunk) or one
 // (m, l, o) partial per (query head, chunk) for merge_kernel.
+//
+// MHA batches of >= 4 requests (CG = 2, tc2_pair_axis): the CTAs of requests 2j and
+// 2j + 1 (same column block and chunk) form a cluster and compute M = 256 rows with
+// tcgen05.mma.cta_group::2, issued by the even CTA into both CTAs' TMEM: each CTA
+// stages its own 128 latent rows and HALF of the 256 U columns per stage (a 4-deep
+// ring of 32 KB instead of 3 x 48 KB, half the L2 reads of U); a relay thread per CTA
+// turns "my stage landed" into a (relaxed) remote arrive on the even CTA's pfull
+// barrier, MMA completion is multicast to both CTAs' empty / tfull barriers, and both
+// epilogues release the accumulator with remote arrives on the even CTA's tempty.
 #include <cuda.h>
 #include <type_traits>
 #include <cudaTypedefs.h>
@@ -244,7 +253,6 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
 
 struct KArgs {
   TcArgs a;
-  int axis;   // (CG = 2) the pair: 1 = consecutive chunks, 3 = consecutive requests
 };
 
 // Split merge fused into the kernel: every chunk CTA of (request b, column block
@@ -388,7 +396,7 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // (C2, pair of requests: the cluster pairs along x, which a cta_group::2 launch needs,
   // so x = 2 chunk + (b & 1), z = b / 2)
-  const bool zpair = C2 && ka.axis == 3;
+  const bool zpair = C2;
   const int chunk = zpair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x, nb = blockIdx.y;
   const int b = zpair ? (int)(2 * blockIdx.z + (blockIdx.x & 1)) : (int)blockIdx.z;
   const int n0 = nb * kBN;
@@ -446,9 +454,8 @@ recon_attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_u, const __grid_c
   const uint32_t crank = C2 ? cluster_ctarank() : 0u;
   int ntile_pair = ntile;
   if constexpr (C2) {
-    const int pchunk = ka.axis == 1 ? (chunk ^ 1) : chunk, pb = ka.axis == 3 ? (b ^ 1) : b;
-    const int pcnt = a.count[pb];
-    const int pt0 = pchunk * a.tiles_per_cta;
+    const int pcnt = a.count[b ^ 1];   // the partner request, same chunk
+    const int pt0 = chunk * a.tiles_per_cta;
     const int pt1 = min((pcnt + kRows - 1) / kRows, pt0 + a.tiles_per_cta);
     ntile_pair = max(ntile, pt1 - pt0);
   }
@@ -1117,7 +1124,7 @@ cudaError_t launch_t(const CUtensorMap& map, const CUtensorMap& map_lat, const C
   at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = CG == 2 ? 2 : 1;
-  KArgs ka{a, axis};
+  KArgs ka{a};
   return cudaLaunchKernelEx(&cfg, kern, map, map_lat, map_v, map_vh, ka);
 }
 
@@ -1125,17 +1132,20 @@ cudaError_t launch_t(const CUtensorMap& map, const CUtensorMap& map_lat, const C
 // pair instead of once per CTA) when the grid pairs up: consecutive chunks, else requests.
 // Opt-in (SALS_TC2_CG=2): parity-green but measured slower than the one-CTA kernel at c2
 // (profiles/r2/experiments).
+// Measured (c5 sweep, 32 layers, one B200, profiles/r2/experiments): with request pairs the
+// pair kernel is 1.00-1.10x the one-CTA kernel from B = 4 up (the most at long contexts and
+// large batches: half the L2 reads of U, a 4-deep operand ring), 0.95-0.98x at B = 1 / 2
+// (chunk pairs / short chains), so it runs for MHA batches of >= 4 requests, paired by
+// request (a pair runs max(tiles) of its CTAs: two requests' same chunk).
 int tc2_pair_axis(const TcArgs& a, int batch) {
   if (!tc2_pair_enabled() || a.G != 1 || a.v_bits != 0) return 0;
-  if (a.ntiles % 2 == 0) return 1;
-  if (batch % 2 == 0) return 3;
-  return 0;
+  return (batch >= 4 && batch % 2 == 0) ? 3 : 0;
 }
 
 }  // namespace tc2
 
-bool tc2_pair_enabled() {
-  static const bool on = [] { const char* e = getenv("SALS_TC2_CG"); return e && e[0] == '2'; }();
+bool tc2_pair_enabled() {   // SALS_TC2_CG=1: the one-CTA kernel for every shape
+  static const bool on = [] { const char* e = getenv("SALS_TC2_CG"); return !(e && e[0] == '1'); }();
   return on;
 }
 
