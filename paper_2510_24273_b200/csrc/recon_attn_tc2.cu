@@ -1129,10 +1129,7 @@ cudaError_t launch_t(const CUtensorMap& map, const CUtensorMap& map_lat, const C
 }
 
 // MHA with bf16 values on a CTA pair (cta_group::2, M = 256: each U tile is read once per
-// pair instead of once per CTA) when the grid pairs up: consecutive chunks, else requests.
-// Opt-in (SALS_TC2_CG=2): parity-green but measured slower than the one-CTA kernel at c2
-// (profiles/r2/experiments).
-// Measured (c5 sweep, 32 layers, one B200, profiles/r2/experiments): with request pairs the
+// pair instead of once per CTA).  Measured (c5 sweep, 32 layers, one B200, profiles/r2/experiments): with request pairs the
 // pair kernel is 1.00-1.10x the one-CTA kernel from B = 4 up (the most at long contexts and
 // large batches: half the L2 reads of U, a 4-deep operand ring), 0.95-0.98x at B = 1 / 2
 // (chunk pairs / short chains), so it runs for MHA batches of >= 4 requests, paired by
