@@ -430,10 +430,11 @@ sals_status launch_flash(const sals_config* c, FlashArgs a, int batch, cudaStrea
 
 template <typename T>
 sals_status launch_merge(const sals_config* c, MergeArgs a, int batch, cudaStream_t st) {
-  // head_dim x SG threads: SG split streams per dim when there are many splits (the dense
-  // comparator's ~148 at B = 1, the fused kernel's 8-32 chunks at c3 / c4)
-  const int sgs = a.nsplit >= 64 ? 4 : (a.nsplit >= 16 ? 2 : 1);
-  const int nt = std::min(1024, std::max(32, c->head_dim * sgs));
+  // head_dim x SG threads (SG <= 8): SG split streams per dim when there are many splits
+  // (the dense comparator's ~148 at B = 1, the fused kernel's 8-32 chunks at c3 / c4)
+  int sgs = a.nsplit >= 128 ? 8 : (a.nsplit >= 64 ? 4 : (a.nsplit >= 16 ? 2 : 1));
+  while (sgs > 1 && c->head_dim * sgs > 1024) sgs >>= 1;
+  const int nt = std::max(32, c->head_dim * sgs);
   SALS_CUDA_TRY(launch(merge_kernel<T>, dim3(batch * c->num_q_heads), dim3(nt), 0, st, 0, a));
   return SALS_OK;
 }

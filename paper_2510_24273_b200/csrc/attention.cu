@@ -308,7 +308,7 @@ __global__ void merge_kernel(MergeArgs a) {
     const int SG = max(1, (int)blockDim.x / a.head_dim);
     const int sg = threadIdx.x / a.head_dim;
     const int i = threadIdx.x - sg * a.head_dim;
-    __shared__ float s_part[3][256];
+    __shared__ float s_part[7][256];
     float acc = 0.f;
     if (sg < SG) {
       const float* po = base + 2 + i;
