@@ -10,8 +10,9 @@
 //      hist0 (one descending block scan over 2048 bins, 2 per thread);
 //  P1-P3  radix passes over key bits [20:13], [12:5], [4:0] of the ranked
 //      entries that share the prefix (smem histogram of 256 bins, digit found
-//      by one warp) -> the full threshold key T and need_eq, the number of
-//      entries equal to T to take;
+//      by one warp) -> the threshold key T and need_eq, the number of entries
+//      equal to T to take; the passes stop as soon as every entry with the
+//      resolved prefix is taken (T is then compared at that prefix's bits);
 //  E   block scan of the per-thread counts of entries equal to T (index order)
 //      -> which ties are taken (the lowest indices);
 //  S   block scan of the per-thread selected counts -> ascending output.
@@ -59,10 +60,10 @@ __device__ __forceinline__ int2 block_excl_scan(int v, int* wsum) {
 }
 
 // Every warp: the digit d of a 256-bin histogram h (descending) such that the
-// entries in bins > d number < need <= those in bins >= d, and need minus the
-// entries in bins > d.  Register-only result (ballot + shuffle broadcast), so
-// no shared flag and no second barrier.
-__device__ __forceinline__ int2 digit_search_all(const uint32_t* h, int need) {
+// entries in bins > d number < need <= those in bins >= d, need minus the entries
+// in bins > d, and the entries in bin d.  Register-only result (ballot + shuffle
+// broadcast), so no shared flag and no second barrier.
+__device__ __forceinline__ int3 digit_search_all(const uint32_t* h, int need) {
   const int lane = threadIdx.x & 31;
   // bins 255 - 8 lane - j, j < 8: two 16-byte loads per lane (conflict-free, the
   // 1 KB histogram in 8 wavefronts; a scalar lane-strided read would be 8-way conflicted)
@@ -81,22 +82,23 @@ __device__ __forceinline__ int2 digit_search_all(const uint32_t* h, int need) {
   int excl = incl - t;
   const bool mine = excl < need && need <= incl;
   const unsigned m = __ballot_sync(0xffffffffu, mine);
-  int d = 0, r = need;
+  int d = 0, r = need, cb = -1;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    if (mine && excl < need && need <= excl + c[j]) { d = 255 - 8 * lane - j; r = need - excl; }
+    if (mine && excl < need && need <= excl + c[j]) { d = 255 - 8 * lane - j; r = need - excl; cb = c[j]; }
     excl += c[j];
   }
   const int src = m ? __ffs(m) - 1 : 0;
-  return make_int2(__shfl_sync(0xffffffffu, d, src), __shfl_sync(0xffffffffu, r, src));
+  return make_int3(__shfl_sync(0xffffffffu, d, src), __shfl_sync(0xffffffffu, r, src),
+                   __shfl_sync(0xffffffffu, cb, src));
 }
 
 template <int EPT>
 __global__ void __launch_bounds__(NT, 1) topk_cta_kernel(TopkArgs a) {
   __shared__ __align__(16) uint32_t hist[3][256];   // one histogram per radix pass (no reuse, no extra barrier)
   __shared__ int wsum[3][65];   // one scratch per block scan
-  __shared__ volatile int s_digit, s_need;
-  __shared__ int2 s_dr[3];
+  __shared__ volatile int s_digit, s_need, s_cnt;
+  __shared__ int3 s_dr[3];
   const int tid = threadIdx.x;
   const int b = blockIdx.x;
   if (tid < 256) { hist[0][tid] = 0; hist[1][tid] = 0; hist[2][tid] = 0; }
@@ -155,11 +157,13 @@ __global__ void __launch_bounds__(NT, 1) topk_cta_kernel(TopkArgs a) {
   const bool take_all = want >= nr;        // every ranked entry selected (also nr == 0)
   const bool take_none = want <= 0;
   const int nd = take_all ? nr : (take_none ? 0 : want);
-  if (tid == 0) { s_digit = -2; s_need = 0; }
+  if (tid == 0) { s_digit = -2; s_need = 0; s_cnt = -1; }
   __syncthreads();
   if (nd > 0 && nd < nr) {
-    if (excl0 < nd && nd <= excl0 + c0) { s_digit = kH0Bins - 1 - 2 * tid; s_need = nd - excl0; }
-    else if (excl0 + c0 < nd && nd <= excl0 + c0 + c1) { s_digit = kH0Bins - 2 - 2 * tid; s_need = nd - excl0 - c0; }
+    if (excl0 < nd && nd <= excl0 + c0) { s_digit = kH0Bins - 1 - 2 * tid; s_need = nd - excl0; s_cnt = c0; }
+    else if (excl0 + c0 < nd && nd <= excl0 + c0 + c1) {
+      s_digit = kH0Bins - 2 - 2 * tid; s_need = nd - excl0 - c0; s_cnt = c1;
+    }
   }
   __syncthreads();
   // T: every ranked key > T is selected, keys == T up to need_eq (index order).
@@ -172,27 +176,35 @@ __global__ void __launch_bounds__(NT, 1) topk_cta_kernel(TopkArgs a) {
   }
   uint32_t prefix = (uint32_t)max(s_digit, 0) << kH0Shift;
   int rem = s_need;
+  // tsh: the key bits below it are not resolved; the passes stop early (block-uniform:
+  // every thread reads the same shared values) once every key with the resolved prefix
+  // is taken (rem == the bin's count), and the selection then compares prefixes
+  int tsh = s_cnt == rem ? kH0Shift : 0;
   TKC_T(3);
   // ---- P1-P3: radix passes over the ranked keys that share the prefix ----
 #pragma unroll
   for (int ps = 0; ps < 3; ++ps) {
-    const int sh = ps == 0 ? 13 : (ps == 1 ? 5 : 0);
-    const uint32_t dmask = ps == 2 ? 31u : 255u;
-    const int hi = sh + (ps == 2 ? 5 : 8);        // bits above this digit are fixed by the prefix
-    uint32_t* h = hist[ps];
+    if (tsh == 0) {
+      const int sh = ps == 0 ? 13 : (ps == 1 ? 5 : 0);
+      const uint32_t dmask = ps == 2 ? 31u : 255u;
+      const int hi = sh + (ps == 2 ? 5 : 8);        // bits above this digit are fixed by the prefix
+      uint32_t* h = hist[ps];
 #pragma unroll
-    for (int j = 0; j < EPT; ++j)
-      if (rk[j] && (key[j] >> hi) == (prefix >> hi)) atomicAdd(&h[(key[j] >> sh) & dmask], 1u);
-    __syncthreads();
-    if (tid < 32) {   // one warp searches, the result is broadcast through shared memory
-      const int2 dr = digit_search_all(h, rem);
-      if (tid == 0) s_dr[ps] = dr;
+      for (int j = 0; j < EPT; ++j)
+        if (rk[j] && (key[j] >> hi) == (prefix >> hi)) atomicAdd(&h[(key[j] >> sh) & dmask], 1u);
+      __syncthreads();
+      if (tid < 32) {   // one warp searches, the result is broadcast through shared memory
+        const int3 dr = digit_search_all(h, rem);
+        if (tid == 0) s_dr[ps] = dr;
+      }
+      __syncthreads();
+      prefix |= (uint32_t)s_dr[ps].x << sh;
+      rem = s_dr[ps].y;
+      if (sh > 0 && s_dr[ps].z == rem) tsh = sh;
     }
-    __syncthreads();
-    prefix |= (uint32_t)s_dr[ps].x << sh;
-    rem = s_dr[ps].y;
   }
-  const uint32_t T = prefix;
+  // T (compared at bits >= tsh): keys above T are selected, keys equal to T up to need_eq
+  const uint32_t T = prefix >> tsh;
   const int need_eq = rem;
 
   TKC_T(4);
@@ -204,8 +216,8 @@ __global__ void __launch_bounds__(NT, 1) topk_cta_kernel(TopkArgs a) {
   int my_eq = 0, my_def = 0;
 #pragma unroll
   for (int j = 0; j < EPT; ++j) {
-    const bool eq = !all_ranked && rk[j] && key[j] == T;
-    const bool def = fc[j] || (rk[j] && (all_ranked || key[j] > T));
+    const bool eq = !all_ranked && rk[j] && (key[j] >> tsh) == T;
+    const bool def = fc[j] || (rk[j] && (all_ranked || (key[j] >> tsh) > T));
     my_eq += eq ? 1 : 0;
     my_def += def ? 1 : 0;
   }
@@ -219,8 +231,8 @@ __global__ void __launch_bounds__(NT, 1) topk_cta_kernel(TopkArgs a) {
     int e = eq_before;
 #pragma unroll
     for (int j = 0; j < EPT; ++j) {
-      const bool eq = !all_ranked && rk[j] && key[j] == T;
-      sl[j] = fc[j] || (rk[j] && (all_ranked || key[j] > T)) || (eq && e < need_eq);
+      const bool eq = !all_ranked && rk[j] && (key[j] >> tsh) == T;
+      sl[j] = fc[j] || (rk[j] && (all_ranked || (key[j] >> tsh) > T)) || (eq && e < need_eq);
       e += eq ? 1 : 0;
     }
   }

@@ -130,6 +130,45 @@ def test_topk_exact_on_kernel_scores(s, npat, sink, recent, k):
         assert (got[b, n:] == -1).all()
 
 
+@pytest.mark.parametrize("s,k,sink,recent", [(4096, 512, 0, 0), (5000, 512, 4, 64), (8000, 1000, 16, 128)])
+def test_topk_threshold_bin_fully_taken(s, k, sink, recent):
+    """Exactly k - x - z ranked tokens share the top score (the rest share a lower one),
+    so the top-digit threshold bin is taken whole and the single-CTA top-k stops its radix
+    passes early (topk_cta.cu): the selection must still equal the oracle's select_topk on
+    the kernel's own scores."""
+    from paper_2510_24273_b200 import sals
+    sh = _shape("c2", num_q_heads=4, num_kv_heads=4, rank=64, score_rank=32, top_k=k)
+    sh.update(sink=sink, recent=recent)
+    cfg = sals.make_config(**sh)
+    B = 2
+    g = torch.Generator(device="cuda"); g.manual_seed(99 + s)
+    U = torch.from_numpy(synth.orthonormal(np.random.default_rng(2), 512, 64).astype(np.float32)).cuda().bfloat16()
+    q = torch.randn(B, 512, device="cuda", generator=g).bfloat16()
+    qt = (q.float() @ U.float())[:, :32]                      # the latent query direction (r* columns)
+    hi = (qt / qt.norm(dim=1, keepdim=True)).repeat(1, 2)     # [B, 64]: large positive score
+    lat = torch.empty(B, s, 64, device="cuda")
+    rng = np.random.default_rng(s)
+    for b in range(B):
+        lat[b] = -0.5 * hi[b]
+        ranked = np.arange(sink, s - recent)
+        pick = rng.choice(ranked, size=k - sink - recent, replace=False)
+        lat[b, torch.from_numpy(pick).cuda()] = 2.0 * hi[b]
+    lat = lat.bfloat16()
+    v = torch.randn(B, s, 512, device="cuda", generator=g).bfloat16()
+    seq = torch.tensor([s, s], dtype=torch.int32, device="cuda")
+    ws = sals.alloc_workspace(sals.sals_workspace_bytes(cfg, B, s), "cuda")
+    out = torch.empty(B, 512, dtype=torch.bfloat16, device="cuda")
+    sel = torch.empty(B, k, dtype=torch.int32, device="cuda")
+    scores = torch.empty(B, s, dtype=torch.float32, device="cuda")
+    sals.sals_decode(cfg, U, q, lat, v, seq, s, out, ws, sel_idx_out=sel, scores_out=scores)
+    torch.cuda.synchronize()
+    sc = scores.cpu().numpy()
+    got = sel.cpu().numpy()
+    for b in range(B):
+        want = O.select_topk(sc[b].astype(np.float64), k, sink=sink, recent=recent)
+        assert np.array_equal(got[b, :len(want)], want), f"request {b}"
+
+
 def test_graph_capture_replay_is_deterministic():
     from paper_2510_24273_b200 import sals
     sh = _shape("c3", rank=256, score_rank=128, top_k=512)
