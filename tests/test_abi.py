@@ -87,6 +87,13 @@ def test_host_validation_without_gpu(lib_path):
     st = sals._lib.sals_decode_sharded(ctypes.byref(cw), fake, fake, fake, fake, fake, 4096, 1, 0, fake, 4096, fake,
                                        fake, fake, 1 << 30, None)
     assert st == 2 and "window" in sals.sals_last_error()
+    # the fused sharded append: NULL k_new / v_new, or a NULL communicator, rejected up front
+    st = sals._lib.sals_append_decode_sharded(ctypes.byref(c), fake, fake, None, None, fake, fake, fake, 4096, 1, 0,
+                                              fake, 4096, fake, fake, fake, 1 << 30, None)
+    assert st == 1
+    st = sals._lib.sals_append_decode_sharded(ctypes.byref(c), None, fake, fake, fake, fake, fake, fake, 4096, 1, 0,
+                                              fake, 4096, fake, fake, fake, 1 << 30, None)
+    assert st == 1 and "communicator" in sals.sals_last_error()
     h = ctypes.c_void_p()
     assert sals._lib.sals_comm_init(ctypes.create_string_buffer(128), 2, 2, ctypes.byref(h)) == 1
     assert sals._lib.sals_comm_destroy(None) == 0
