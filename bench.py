@@ -252,7 +252,12 @@ def run_reference(args, rank, world):
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": describe(args.workload, sh, L), "batch": B, "seq_len": sh["seq"], "layers": L},
+            # the same config dict as this bench's own line for the workload (the default run's
+            # headline is c2), so the two arms name the identical workload
+            "config": {"workload": describe("c2" if args.workload == "all" else args.workload, sh, L), "batch": B,
+                       "seq_len": sh["seq"], "layers": L,
+                       "l2": "inputs larger than L2: 32 distinct layers' caches per step",
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
                              "sample": f"each step = 1 request x 1 layer oracle append+decode at the full workload "
                                        f"shape (median of {args.steps}), extrapolated x{B} requests x{L} layers"},
